@@ -1,0 +1,130 @@
+/*
+ * lf_b200.h — C ABI of the B200-native CKKS core (libcerium_b200.so).
+ *
+ * This is the drop-in boundary under the reference's Python operator API
+ * (`limbforge.ckks`, /root/reference/pkg/src/limbforge/ckks.py:59-225, re-exported at
+ * __init__.py:10-34).  The Python host layer `paper_2512_11269_b200` mirrors that API
+ * function for function and calls the entry points below through ctypes; a foreign host
+ * (cgo, JNI, N-API) would bind the same symbols.
+ *
+ * Conventions
+ *  - Every function returns 0 on success, non-zero on failure; lf_last_error() describes
+ *    the last failure of the calling thread.
+ *  - Residues are uint32 (primes < 2^28, reference params.py:14-16), stored limb-major:
+ *    a polynomial over n basis primes is n contiguous rows of N words.
+ *  - All data pointers are DEVICE pointers owned by the caller; `stream` is a
+ *    cudaStream_t passed as void*.  Calls are asynchronous on that stream, never
+ *    synchronise the host, and never allocate (workspace is passed in), except
+ *    lf_ctx_create / lf_ctx_destroy.
+ *  - Metadata arrays (prime indices, scalars) are HOST arrays; `prime_idx[r]` indexes the
+ *    context's prime list (main primes 0..L, then special primes L+1..L+alpha).
+ *  - Canonical residues in, canonical residues out; `out` may alias inputs unless noted.
+ */
+#ifndef LF_B200_H
+#define LF_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct LfCtx lf_ctx;
+
+#define LF_ABI_VERSION 1
+
+/* element-wise op codes (reference poly.py:85-117) */
+#define LF_OP_ADD 0            /* a + b                 row_add      poly.py:85   */
+#define LF_OP_SUB 1            /* a - b                 row_sub      poly.py:89   */
+#define LF_OP_MUL 2            /* a * b                 row_mul      poly.py:94   */
+#define LF_OP_NEG 3            /* -a                    row_neg      poly.py:104  */
+#define LF_OP_SCALAR_MUL 4     /* a * s_r               row_scalar_mul poly.py:108 */
+#define LF_OP_MULACC 5         /* c + a * b             row_mulacc   poly.py:98   */
+#define LF_OP_MODSTEP 6        /* (a - b) * s_r         row_modstep  poly.py:112  */
+#define LF_OP_MUL_SCALAR_ADD 7 /* a * s_r + b           (fused helper)            */
+
+int lf_abi_version(void);
+const char* lf_last_error(void);
+
+/* Context: per-prime constants and twiddle tables for ring dimension N = 2^logN.
+ * psis[i] is the primitive 2N-th root used by the reference (modmath.py:61-68: smallest
+ * generator g, psi = g^((q-1)/2N)); tables follow ntt.py:22-67.  Replaces the reference's
+ * ntt_tables() cache (ntt.py:44-67). */
+int lf_ctx_create(int logN, int nprimes, const uint32_t* primes, const uint32_t* psis,
+                  lf_ctx** out);
+int lf_ctx_destroy(lf_ctx* ctx);
+
+/* Batched negacyclic NTT, in place.  Replaces ntt_forward / ntt_inverse (ntt.py:70-105)
+ * and poly_ntt / poly_intt (poly.py:212-225).  Output of lf_ntt_fwd is in the reference's
+ * bit-reversed evaluation order. */
+int lf_ntt_fwd(const lf_ctx* ctx, uint32_t* rows, int nrows, const int32_t* prime_idx,
+               void* stream);
+int lf_ntt_inv(const lf_ctx* ctx, uint32_t* rows, int nrows, const int32_t* prime_idx,
+               void* stream);
+
+/* Element-wise row primitives (poly.py:85-117, 183-209).  b, c may be NULL when the op does
+ * not read them; scalars (host, one per row, reduced mod the row's prime) may be NULL. */
+int lf_ewise(const lf_ctx* ctx, int op, uint32_t* out, const uint32_t* a, const uint32_t* b,
+             const uint32_t* c, int nrows, const int32_t* prime_idx, const uint32_t* scalars,
+             void* stream);
+
+/* Evaluation-domain automorphism X -> X^g on nrows rows: out[i] = in[perm_g(i)]
+ * (ntt.py:108-126, poly.py:120-121, 228-231).  g odd.  out must not alias in. */
+int lf_automorph(const lf_ctx* ctx, uint32_t* out, const uint32_t* in, uint32_t g, int nrows,
+                 void* stream);
+
+/* Exact base conversion of coefficient-domain rows (poly.py:150-178): src holds k rows,
+ * out receives m rows.  `table` is a device blob laid out as described in DESIGN.md
+ * ("BConv table") and built by the host (paper_2512_11269_b200/plan.py). */
+int lf_bconv(const lf_ctx* ctx, uint32_t* out, const uint32_t* src, const uint32_t* table,
+             int k, int m, int W, void* stream);
+
+/* ---- fused hybrid keyswitch pipeline ---------------------------------------------------
+ * lf_ctx_enable_keyswitch builds, once, every constant of the keyswitch / rescale path for a
+ * context whose first n_main primes are the main basis q_0..q_L and the rest the special
+ * basis (reference params.py:117-131), with d round-robin digits (params.py:23-41).
+ *
+ * Layouts (uint32 words, rows of N):
+ *   x            level+1 rows                       (one polynomial, eval domain)
+ *   ciphertext   2 x (level+1) rows: b rows then a rows      (ckks.py:40-50)
+ *   evk          d x 2 x (L+1+alpha) rows: digit j, (b, a), extended-basis row (keys.py:40-49)
+ *   out          2 x (level+1) rows (ks_b then ks_a, or b' then a')
+ * Batched calls process `batch` independent instances; *_bstride are the word strides
+ * between instances (0 = shared, e.g. one relinearisation key for the whole batch).
+ * workspace: lf_ks_workspace_bytes(ctx, level, batch) bytes of device memory. */
+int lf_ctx_enable_keyswitch(lf_ctx* ctx, int n_main, int d);
+size_t lf_ks_workspace_bytes(const lf_ctx* ctx, int level, int batch);
+
+/* keyswitch(x, evk) -> (ks_b, ks_a) over the main ids of x's level.
+ * Replaces ckks.keyswitch (ckks.py:134-140) = keyswitch_decompose (ckks.py:95-117) +
+ * keyswitch_inner_product (ckks.py:120-131) + mod_down x2 (poly.py:251-281). */
+int lf_keyswitch(const lf_ctx* ctx, int level, const uint32_t* x, size_t x_bstride,
+                 const uint32_t* evk, size_t evk_bstride, uint32_t* out, size_t out_bstride,
+                 int batch, void* workspace, void* stream);
+
+/* hom_mul (ckks.py:182-194): tensor product + relinearisation, no rescale. */
+int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t* ct2,
+               size_t ct_bstride, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
+               int batch, void* workspace, void* stream);
+
+/* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
+ * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a
+ * rotation, 2N-1 for conjugation. */
+int lf_rotate(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride, uint32_t g,
+              const uint32_t* key, size_t key_bstride, uint32_t* out, size_t out_bstride,
+              int batch, void* workspace, void* stream);
+
+/* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
+size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
+int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,
+               uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
+
+/* keyswitch_decompose (ckks.py:95-117) materialised: pieces = beta x (level+1+alpha) rows,
+ * eval domain, digit-major; beta = min(d, level+1).  Workspace as lf_keyswitch (batch 1). */
+int lf_ks_decompose(const lf_ctx* ctx, int level, const uint32_t* x, uint32_t* pieces,
+                    void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LF_B200_H */

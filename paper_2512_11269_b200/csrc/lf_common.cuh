@@ -1,0 +1,55 @@
+// Shared host/device declarations of the B200 CKKS core.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "lf_arith.cuh"
+#include "lf_line.cuh"
+
+// Device view of one parameter context (all tables resident in HBM).
+struct LfDev {
+  const PrimeK* pk;      // [nprimes]  per-prime constants
+  const uint2* twf;      // [nprimes << logN]  {psi^brv(i), Shoup companion}
+  const uint2* twi;      // [nprimes << logN]  {psi^-brv(i), Shoup companion}
+  int logN;
+  int nprimes;
+};
+
+// Prime index of each row of a row batch (rows are N contiguous words each).
+#define LF_MAX_ROWS 256
+struct RowMap {
+  int n;
+  unsigned char p[LF_MAX_ROWS];
+};
+
+struct LfKsPlan;
+struct LfCtx {
+  int logN, N, nprimes;
+  LfKsPlan* ks;          // keyswitch plans (lf_ctx_enable_keyswitch), or null
+  PrimeK* d_pk;
+  uint2* d_twf;
+  uint2* d_twi;
+  PrimeK* h_pk;
+  LfDev dev() const { return LfDev{d_pk, d_twf, d_twi, logN, nprimes}; }
+};
+
+// error plumbing (lf_api.cu)
+void lf_set_error(const char* fmt, ...);
+#define LF_CHECK_LAUNCH()                                                  \
+  do {                                                                     \
+    cudaError_t e__ = cudaGetLastError();                                  \
+    if (e__ != cudaSuccess) {                                              \
+      lf_set_error("%s:%d: %s", __FILE__, __LINE__, cudaGetErrorString(e__)); \
+      return 3;                                                            \
+    }                                                                      \
+  } while (0)
+
+// split of logN into column-pass (L1) and row-pass (L2) stage counts
+inline void lf_split(int logN, int& L1, int& L2) {
+  L1 = logN / 2;
+  L2 = logN - L1;
+}
+
+// host launchers (lf_ntt.cu)
+int lf_launch_ntt(const LfCtx* ctx, u32* rows, const RowMap& rm, bool inverse, cudaStream_t s);

@@ -1,0 +1,130 @@
+// Row primitives (reference poly.py:85-121) and the coefficient-domain exact base conversion
+// (poly.py:150-178, 234-248) on row batches.  Rows are N contiguous uint32 words; row r uses
+// prime rm.p[r].  All outputs are canonical residues; `out` may alias any input.
+#include "lf_ntt.cuh"
+#include "lf_bconv.cuh"
+#include "lf_ops.h"
+
+struct EwArgs {
+  u32* out;
+  const u32* a;
+  const u32* b;
+  const u32* c;
+  int op;
+  RowMap rm;
+  u32 s[LF_MAX_ROWS];
+  u32 sp[LF_MAX_ROWS];
+};
+
+LF_DEV u32 ew_one(int op, u32 a, u32 b, u32 c, u32 s, u32 sp, const PrimeK& k) {
+  const u32 q = k.q;
+  switch (op) {
+    case LF_OP_ADD: return addmod(a, b, q);
+    case LF_OP_SUB: return submod(a, b, q);
+    case LF_OP_MUL: return mulmod(a, b, k);
+    case LF_OP_NEG: return a ? q - a : 0u;
+    case LF_OP_SCALAR_MUL: return mul_shoup(a, s, sp, q);
+    case LF_OP_MULACC: return reduce64((u64)a * b + c, k);
+    case LF_OP_MODSTEP: return mul_shoup(submod(a, b, q), s, sp, q);
+    case LF_OP_MUL_SCALAR_ADD: return addmod(mul_shoup(a, s, sp, q), b, q);   // a*s + b
+    default: return 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ewise(EwArgs A, LfDev dv, int logN) {
+  const int row = blockIdx.y;
+  const PrimeK k = dv.pk[A.rm.p[row]];
+  const u32 s = A.s[row], sp = A.sp[row];
+  const size_t N = (size_t)1 << logN;
+  const size_t nv = N / 4;
+  const size_t off = row * N;
+  const uint4* a4 = reinterpret_cast<const uint4*>(A.a + off);
+  const uint4* b4 = A.b ? reinterpret_cast<const uint4*>(A.b + off) : nullptr;
+  const uint4* c4 = A.c ? reinterpret_cast<const uint4*>(A.c + off) : nullptr;
+  uint4* o4 = reinterpret_cast<uint4*>(A.out + off);
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < nv;
+       v += (size_t)gridDim.x * blockDim.x) {
+    const uint4 a = a4[v];
+    const uint4 b = b4 ? b4[v] : make_uint4(0, 0, 0, 0);
+    const uint4 c = c4 ? c4[v] : make_uint4(0, 0, 0, 0);
+    uint4 o;
+    o.x = ew_one(A.op, a.x, b.x, c.x, s, sp, k);
+    o.y = ew_one(A.op, a.y, b.y, c.y, s, sp, k);
+    o.z = ew_one(A.op, a.z, b.z, c.z, s, sp, k);
+    o.w = ew_one(A.op, a.w, b.w, c.w, s, sp, k);
+    o4[v] = o;
+  }
+}
+
+// out[r][i] = in[r][perm_g(i)]   (out must not alias in)
+__global__ void __launch_bounds__(256) k_automorph(u32* out, const u32* in, u32 g, int logN,
+                                                   int nrows) {
+  const size_t N = (size_t)1 << logN;
+  const size_t total = N * nrows;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = idx >> logN;
+    const u32 i = (u32)(idx & (N - 1));
+    out[idx] = in[(row << logN) + auto_src_index(i, g, logN)];
+  }
+}
+
+// Coefficient-domain exact conversion: src (k rows) -> out (m rows), one thread per coeff.
+__global__ void __launch_bounds__(128) k_bconv(u32* out, const u32* src, BconvDev B, LfDev dv) {
+  const size_t N = (size_t)1 << dv.logN;
+  const size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  u32 y[64];
+  for (int i = 0; i < B.k; ++i) {
+    const PrimeK ks = dv.pk[B.src_pi[i]];
+    y[i] = mul_shoup(src[i * N + n] % ks.q, B.c[i], B.cp[i], ks.q);
+  }
+  const u32 u = bconv_u(y, B);
+  for (int t = 0; t < B.m; ++t) {
+    const PrimeK kt = dv.pk[B.tgt_pi[t]];
+    u64 acc = (u64)u * B.negS[t];
+    for (int i = 0; i < B.k; ++i) acc += (u64)y[i] * B.w[(size_t)t * B.k + i];
+    out[t * N + n] = reduce64(acc, kt);
+  }
+}
+
+int lf_launch_ewise(const LfCtx* ctx, int op, u32* out, const u32* a, const u32* b,
+                    const u32* c, const RowMap& rm, const u32* scalars, cudaStream_t s) {
+  EwArgs A;
+  A.out = out; A.a = a; A.b = b; A.c = c; A.op = op; A.rm = rm;
+  for (int r = 0; r < rm.n; ++r) {
+    const u32 q = ctx->h_pk[rm.p[r]].q;
+    const u32 v = scalars ? scalars[r] % q : 0u;
+    A.s[r] = v;
+    A.sp[r] = (u32)(((u64)v << 32) / q);
+  }
+  const int nv = ctx->N / 4;
+  const int bx = (nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64;
+  dim3 grid(bx, rm.n);
+  k_ewise<<<grid, 256, 0, s>>>(A, ctx->dev(), ctx->logN);
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
+int lf_launch_automorph(const LfCtx* ctx, u32* out, const u32* in, u32 g, int nrows,
+                        cudaStream_t s) {
+  const size_t total = (size_t)ctx->N * nrows;
+  size_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_automorph<<<(unsigned)blocks, 256, 0, s>>>(out, in, g, ctx->logN, nrows);
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
+int lf_launch_bconv(const LfCtx* ctx, u32* out, const u32* src, const u32* tab, int k, int m,
+                    int W, cudaStream_t s) {
+  if (k > 64 || W > LF_BC_MAXW) {
+    lf_set_error("bconv: k=%d W=%d exceeds limits", k, W);
+    return 2;
+  }
+  const BconvDev B = lf_bconv_view(tab, k, m, W);
+  const int blocks = (ctx->N + 127) / 128;
+  k_bconv<<<blocks, 128, 0, s>>>(out, src, B, ctx->dev());
+  LF_CHECK_LAUNCH();
+  return 0;
+}

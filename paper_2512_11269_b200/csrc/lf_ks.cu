@@ -1,0 +1,695 @@
+// Fused hybrid keyswitch pipeline (reference ckks.py:95-140, poly.py:251-287) and the ops
+// built on it: hom_mul (ckks.py:182-194), hom_rotate (ckks.py:197-217), rescale
+// (ckks.py:220-225).
+//
+// With N = 2^L1 * 2^L2 (see lf_line.cuh) one keyswitch of x at level l is five kernels:
+//   K_A  modup_in     row pass of INTT(x)            x (l+1 rows)           -> T0 (l+1)
+//                     [hom_mul: x = a1*a2 formed on load]
+//   K_BC bconv_colpass column pass of INTT, exact BConv of each digit onto ext \ G_j,
+//                     column pass of the NTT          T0                     -> T1 (beta x ext)
+//   K_C  ks_inner     row pass of the NTT of every piece row, automorphism (rotate),
+//                     inner product with the key over all digits (64-bit lazy sums);
+//                     main rows -> ACC, special rows -> row pass of their INTT -> T2
+//   K_BC bconv_colpass (ModDown) column pass of INTT(special rows), BConv onto main primes,
+//                     column pass of the NTT          T2 (2 alpha)           -> T3 (2 (l+1))
+//   K_E  moddown_out  row pass of the NTT, (acc - conv) * P^-1, epilogue
+//                     [hom_mul: + d0/d1; rotate: + sigma_g(b)]            -> out (2 (l+1))
+// Every pass works on whole lines held in registers, so each intermediate row crosses HBM
+// (or L2) once per kernel boundary.  All kernels take a batch dimension (grid.z).
+#include "lf_ntt.cuh"
+#include "lf_bconv.cuh"
+#include "lf_plan.h"
+#include "lf_ops.h"
+
+#define LF_BC_MAXG 16
+
+struct BcArgs {
+  const u32* src;
+  u32* dst;
+  size_t src_bs, dst_bs;     // batch strides (words)
+  int ngroups, tsplit;
+  BcGroupDev g[LF_BC_MAXG];
+};
+
+// ---------------------------------------------------------------------------------------
+// K_A: row pass of the inverse NTT.  MODE 0: rows of x; MODE 1: rows of a1*a2 (tensor d2).
+template <int L1, int L2, int MODE>
+__global__ void __launch_bounds__(NttShape<L1, L2>::TR)
+k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
+           size_t x_bs, size_t t_bs, int nrows, LfDev dv, int src_rs, int src_r0, int pfix) {
+  using S = NttShape<L1, L2>;
+  using C = LineCfg<L2>;
+  extern __shared__ u32 sm[];
+  const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
+  const int nlines = nrows << L1;
+  int line = blockIdx.x * S::LPC + ln;
+  const bool valid = line < nlines;
+  if (!valid) line = nlines - 1;
+  const int row = line >> L1, hi = line & ((1 << L1) - 1);
+  const int pi = pfix >= 0 ? pfix : row;
+  const PrimeK pk = dv.pk[pi];
+  const uint2* tw = dv.twi + ((size_t)pi << (L1 + L2));
+  const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)(row * src_rs + src_r0) << (L1 + L2)) +
+                     ((size_t)hi << L2);
+  u32 v[C::E];
+  load_row_step2<L2>(v, x + off, tl);
+  if (MODE == 1) {
+    u32 w[C::E];
+    load_row_step2<L2>(w, x2 + off, tl);
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
+  }
+  inv_line<L2>(v, (1u << L1) + hi, tw, pk.q, sm, tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
+  if (valid) store_row_step1<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)line << L2), tl);
+}
+
+// ---------------------------------------------------------------------------------------
+// K_BC: column pass of INTT on k source rows, exact BConv, column pass of NTT per target.
+LF_DEV u32 bconv_u_smem(const u32* Yp, int ystride, const BconvDev& B) {
+  double v = 0.0;
+  for (int i = 0; i < B.k; ++i) v = fma((double)Yp[i * ystride], B.inv_s[i], v);
+  const double r = rint(v);
+  if (fabs(v - r) >= 0x1p-40) return (u32)floor(v);
+  u32 y[64];
+  bool z = true;
+  for (int i = 0; i < B.k; ++i) {
+    y[i] = Yp[i * ystride];
+    z &= y[i] == 0;
+  }
+  if (z) return 0;
+  return bconv_u_exact(y, B, (u32)r);
+}
+
+template <int L1, int L2, int CW>
+__global__ void __launch_bounds__(CW * LineCfg<L1>::T)
+k_bconv_colpass(BcArgs A, LfDev dv, int kmax) {
+  using C = LineCfg<L1>;
+  constexpr int M1 = C::M;
+  extern __shared__ u32 sm[];
+  u32* Y = sm;                                   // [kmax][M1][CW]
+  u32* X = sm + (size_t)kmax * M1 * CW;          // exchange
+  const BcGroupDev& G = A.g[blockIdx.y / A.tsplit];
+  const int ts = blockIdx.y % A.tsplit;
+  const BconvDev& B = G.B;
+  const int c = threadIdx.x % CW, tl = threadIdx.x / CW;
+  const int col = blockIdx.x * CW + c;
+  const u32* src = A.src + (size_t)blockIdx.z * A.src_bs;
+  u32* dst = A.dst + (size_t)blockIdx.z * A.dst_bs;
+  const AddrC<L1, CW> addr{c};
+  const int logN = L1 + L2;
+
+  // phase 1: INTT column pass of every source row, y_i = r_i * c_i mod s_i into shared memory
+  for (int i = 0; i < B.k; ++i) {
+    const int pi = B.src_pi[i];
+    const PrimeK pk = dv.pk[pi];
+    const u32* s = src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col;
+    u32 x[C::E];
+    load_col_step2<L1, L2>(x, s, tl);
+    inv_line<L1>(x, 1u, dv.twi + ((size_t)pi << logN), pk.q, X, tl, addr, SyncBlock{});
+    const u32 ci = B.c[i], cpi = B.cp[i];
+#pragma unroll
+    for (int j = 0; j < C::E; ++j)
+      Y[((size_t)i * M1 + tl + C::T * j) * CW + c] = mul_shoup(x[j], ci, cpi, pk.q);
+    __syncthreads();
+  }
+  // phase 2: exact overflow counts for this thread's positions
+  u32 u[C::E];
+#pragma unroll
+  for (int j = 0; j < C::E; ++j)
+    u[j] = bconv_u_smem(Y + (size_t)(tl + C::T * j) * CW + c, M1 * CW, B);
+
+  // phase 3: per target: BConv -> NTT column pass -> T1
+  const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
+  const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
+  for (int t = t0; t < t1; ++t) {
+    const int pi = B.tgt_pi[t];
+    const PrimeK pk = dv.pk[pi];
+    const u32* wt = B.w + (size_t)t * B.k;
+    const u32 ns = B.negS[t];
+    u32 x[C::E];
+#pragma unroll
+    for (int j = 0; j < C::E; ++j) {
+      const u32* yp = Y + (size_t)(tl + C::T * j) * CW + c;
+      u64 acc = (u64)u[j] * ns;
+      for (int i = 0; i < B.k; ++i) acc += (u64)yp[(size_t)i * M1 * CW] * __ldg(&wt[i]);
+      x[j] = reduce64(acc, pk);
+    }
+    fwd_line<L1, 1>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, SyncBlock{});
+    store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K_C: inner product over digits (+ automorphism), ACC / T2 outputs.
+struct KsInnerArgs {
+  const u32* T1;       // beta x ext rows
+  const u32* x;        // own rows source (x, or a1 for the tensor mode)
+  const u32* x2;       // a2 (tensor mode)
+  const u32* key;      // (d, 2, R, N)
+  u32* acc;            // 2 x (l+1) rows
+  u32* T2;             // 2 x alpha rows
+  size_t t1_bs, x_bs, key_bs, acc_bs, t2_bs;
+  const u32* rowk;     // plan: per main row {s, s', pinv, pinv'}
+  int level, d, beta, L, alpha, R;
+  u32 g;               // galois element (GALOIS mode)
+};
+
+template <int L1, int L2, bool GALOIS, int XMODE>
+__global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
+k_ks_inner(KsInnerArgs A, LfDev dv) {
+  using S = NttShape<L1, L2>;
+  using C = LineCfg<L2>;
+  constexpr int M2 = C::M;
+  constexpr int logN = L1 + L2;
+  constexpr int BIN = S::FWD_C_OUT;
+  extern __shared__ u32 sm[];
+  const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
+  const int groups = (1 << L1) / S::LPCR;
+  const int t = blockIdx.x / groups;                         // ext position
+  const int hi = (blockIdx.x % groups) * S::LPCR + ln;
+  const int l = A.level;
+  const bool is_main = t <= l;
+  const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index == key row
+  const PrimeK pk = dv.pk[pi];
+  const int ext = l + 1 + A.alpha;
+  u32* xs = sm + ln * (pitchR<L2>() + M2);
+  u32* perm_buf = xs + pitchR<L2>();
+  const AddrR<L2> addr{0};
+  const size_t b = blockIdx.z;
+
+  int hs = hi;
+  if (GALOIS) hs = (int)(auto_src_index((u32)hi << L2, A.g, logN) >> L2);
+
+  u64 accb[C::E], acca[C::E];
+#pragma unroll
+  for (int e = 0; e < C::E; ++e) { accb[e] = 0; acca[e] = 0; }
+
+  for (int j = 0; j < A.beta; ++j) {
+    u32 pc[C::E];
+    if (is_main && (t % A.d) == j) {
+      // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
+      const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
+      const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
+      const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)t << logN);
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) {
+        const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+        const u32 src = GALOIS ? auto_src_index(pos, A.g, logN) : pos;
+        u32 v = xr[src];
+        if (XMODE == 1) v = mulmod(v, xr2[src], pk);
+        pc[e] = mul_shoup_lazy(v, s, sp, pk.q);
+      }
+    } else {
+      const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
+      load_row_step1<L2>(pc, tr, tl);
+      fwd_line<L2, BIN>(pc, (1u << L1) + hs, dv.twf + ((size_t)pi << logN), pk.q, xs, tl, addr,
+                        SyncWarp{});
+      if (GALOIS) {
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) {
+          const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+          pc[e] = perm_buf[auto_src_index(pos, A.g, logN) & (M2 - 1)];
+        }
+      }
+    }
+    if (A.beta > 15) {
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) pc[e] = reduce32_lazy(pc[e], pk);
+    }
+    const u32* kb = A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2);
+    const u32* ka = A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2);
+    u32 kv[C::E];
+    load_row_step2<L2>(kv, kb, tl);
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kv[e];
+    load_row_step2<L2>(kv, ka, tl);
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kv[e];
+  }
+  u32 rb[C::E], ra[C::E];
+#pragma unroll
+  for (int e = 0; e < C::E; ++e) { rb[e] = reduce64(accb[e], pk); ra[e] = reduce64(acca[e], pk); }
+  if (is_main) {
+    store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2), tl);
+  } else {
+    const int s = t - l - 1;
+    const uint2* tw = dv.twi + ((size_t)pi << logN);
+    __syncwarp();
+    inv_line<L2>(rb, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
+    store_row_step1<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
+    __syncwarp();
+    inv_line<L2>(ra, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
+    store_row_step1<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K_E: row pass of the NTT of the converted rows, (acc - conv) * scalar, epilogue.
+enum { EPI_KS = 0, EPI_MUL = 1, EPI_ROT = 2 };
+struct ModDownArgs {
+  const u32* T3;       // 2 x nt rows (pass-C output)
+  const u32* acc;      // 2 x nacc rows (canonical, eval); row t of poly p at p*nacc + t
+  u32* out;            // 2 x nt rows
+  const u32* e0;       // epilogue inputs (ct1 for MUL: b1 | a1 ; ct for ROT)
+  const u32* e1;       // ct2 for MUL
+  size_t t3_bs, acc_bs, out_bs, e_bs;
+  const u32* scal;     // per target t: scalar, Shoup companion at scal[t*sstride], +1
+  int sstride;
+  int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
+  u32 g;
+};
+
+template <int L1, int L2, int EPI>
+__global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
+k_moddown_out(ModDownArgs A, LfDev dv) {
+  using S = NttShape<L1, L2>;
+  using C = LineCfg<L2>;
+  constexpr int logN = L1 + L2;
+  constexpr int BIN = S::FWD_C_OUT;
+  extern __shared__ u32 sm[];
+  const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
+  const int groups = (1 << L1) / S::LPCR;
+  const int t = blockIdx.x / groups;
+  const int hi = (blockIdx.x % groups) * S::LPCR + ln;
+  const PrimeK pk = dv.pk[t];
+  const u32 sc = A.scal[t * A.sstride], scp = A.scal[t * A.sstride + 1];
+  const uint2* tw = dv.twf + ((size_t)t << logN);
+  const AddrR<L2> addr{ln * pitchR<L2>()};
+  const size_t b = blockIdx.z;
+  const size_t lo0 = ((size_t)hi << L2);
+#pragma unroll 1
+  for (int p = 0; p < 2; ++p) {
+    u32 cv[C::E], av[C::E];
+    load_row_step1<L2>(cv, A.T3 + b * A.t3_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
+    if (p) __syncwarp();
+    fwd_line<L2, BIN>(cv, (1u << L1) + hi, tw, pk.q, sm, tl, addr, SyncWarp{});
+    load_row_step2<L2>(av, A.acc + b * A.acc_bs + ((size_t)(p * A.nacc + t) << logN) + lo0, tl);
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) {
+      const u32 v = av[e] + 8 * pk.q - csub(cv[e], 8 * pk.q);     // (0, 9q)
+      av[e] = mul_shoup(v, sc, scp, pk.q);
+    }
+    if (EPI == EPI_MUL) {
+      // d0 = b1*b2 ; d1 = b1*a2 + a1*b2  (ckks.py:189-193)
+      const u32* c1 = A.e0 + b * A.e_bs;
+      const u32* c2 = A.e1 + b * A.e_bs;
+      u32 b1[C::E], b2[C::E], o1[C::E], o2[C::E];
+      load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo0, tl);
+      load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo0, tl);
+      if (p == 0) {
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) av[e] = addmod(av[e], mulmod(b1[e], b2[e], pk), pk.q);
+      } else {
+        load_row_step2<L2>(o1, c1 + ((size_t)(A.ne + t) << logN) + lo0, tl);
+        load_row_step2<L2>(o2, c2 + ((size_t)(A.ne + t) << logN) + lo0, tl);
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) {
+          const u32 d1 = reduce64((u64)b1[e] * o2[e] + (u64)o1[e] * b2[e], pk);
+          av[e] = addmod(av[e], d1, pk.q);
+        }
+      }
+    } else if (EPI == EPI_ROT) {
+      if (p == 0) {
+        const u32* br = A.e0 + b * A.e_bs + ((size_t)t << logN);
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) {
+          const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+          av[e] = addmod(av[e], br[auto_src_index(pos, A.g, logN)], pk.q);
+        }
+      }
+    }
+    store_row_step2<L2>(av, A.out + b * A.out_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Materialised pieces (keyswitch_decompose API): finish the NTT of T1 rows, own rows x*s.
+template <int L1, int L2>
+__global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
+k_pieces(const u32* __restrict__ T1, const u32* __restrict__ x, u32* __restrict__ out,
+         const u32* rowk, int level, int d, int L, int alpha, LfDev dv) {
+  using S = NttShape<L1, L2>;
+  using C = LineCfg<L2>;
+  constexpr int logN = L1 + L2;
+  extern __shared__ u32 sm[];
+  const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
+  const int groups = (1 << L1) / S::LPCR;
+  const int ext = level + 1 + alpha;
+  const int r = blockIdx.x / groups;          // j * ext + t
+  const int j = r / ext, t = r % ext;
+  const int hi = (blockIdx.x % groups) * S::LPCR + ln;
+  const bool is_main = t <= level;
+  const int pi = is_main ? t : L + 1 + (t - level - 1);
+  const PrimeK pk = dv.pk[pi];
+  const size_t lo0 = (size_t)hi << L2;
+  u32 v[C::E];
+  if (is_main && t % d == j) {
+    load_row_step2<L2>(v, x + ((size_t)t << logN) + lo0, tl);
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) v[e] = mul_shoup(v[e], rowk[4 * t], rowk[4 * t + 1], pk.q);
+  } else {
+    load_row_step1<L2>(v, T1 + ((size_t)r << logN) + lo0, tl);
+    fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi, dv.twf + ((size_t)pi << logN), pk.q, sm, tl,
+                               AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) v[e] = reduce32(v[e], pk);
+  }
+  store_row_step2<L2>(v, out + ((size_t)r << logN) + lo0, tl);
+}
+
+// =======================================================================================
+// host side
+struct KsWs {
+  u32 *T0, *T1, *acc, *T2, *T3;
+  size_t per;    // words per batch instance
+};
+
+static size_t ks_ws_rows(const LfKsPlan* P, int level) {
+  const int l1 = level + 1, ext = l1 + P->n_special;
+  const int beta = P->d < l1 ? P->d : l1;
+  return (size_t)l1 + (size_t)beta * ext + 2 * (size_t)l1 + 2 * (size_t)P->n_special + 2 * (size_t)l1;
+}
+
+static KsWs carve(const LfCtx* ctx, int level, void* ws) {
+  const LfKsPlan* P = ctx->ks;
+  const int l1 = level + 1, ext = l1 + P->n_special;
+  const int beta = P->d < l1 ? P->d : l1;
+  const size_t N = ctx->N;
+  KsWs w;
+  u32* p = (u32*)ws;
+  w.T0 = p; p += (size_t)l1 * N;
+  w.T1 = p; p += (size_t)beta * ext * N;
+  w.acc = p; p += 2 * (size_t)l1 * N;
+  w.T2 = p; p += 2 * (size_t)P->n_special * N;
+  w.T3 = p; p += 2 * (size_t)l1 * N;
+  w.per = ks_ws_rows(P, level) * N;
+  return w;
+}
+
+template <int L1, int L2, int CW>
+static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
+  const size_t sm = ((size_t)kmax * LineCfg<L1>::M * CW + smemC_words<L1, CW>()) * 4;
+  if (sm > 227 * 1024) { lf_set_error("bconv: shared memory %zu too large", sm); return 2; }
+  auto kern = k_bconv_colpass<L1, L2, CW>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((1 << L2) / CW, A.ngroups * A.tsplit, batch);
+  kern<<<grid, CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax);
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
+template <int L1, int L2>
+static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
+  constexpr int NCOL = 1 << L2;
+  // columns per CTA: 8 when the source tile fits, fewer for large digit sizes
+  const size_t per_col = (size_t)kmax * LineCfg<L1>::M * 4;
+  if (NCOL >= 8 && per_col * 8 <= 160 * 1024) return launch_bc<L1, L2, (NCOL >= 8 ? 8 : 1)>(ctx, A, batch, kmax, s);
+  if (NCOL >= 4 && per_col * 4 <= 200 * 1024) return launch_bc<L1, L2, (NCOL >= 4 ? 4 : 1)>(ctx, A, batch, kmax, s);
+  if (NCOL >= 2 && per_col * 2 <= 210 * 1024) return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1)>(ctx, A, batch, kmax, s);
+  return launch_bc<L1, L2, 1>(ctx, A, batch, kmax, s);
+}
+
+static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax) {
+  // expose enough CTAs to fill 148 SMs a few times over; each split redoes the INTT prologue
+  int ts = 1;
+  while (ts < 8 && (long)ngroups * batch * ncoltiles * ts < 148 * 4 && mmax / (ts * 2) >= 6) ts *= 2;
+  return ts;
+}
+
+enum { OP_KS = 0, OP_MUL = 1, OP_ROT = 2 };
+
+struct KsCall {
+  int level, batch, op;
+  const u32 *x, *x2;        // K_A/K_C inputs: x (op KS: the poly; MUL: a1, a2; ROT: ct.a)
+  size_t x_bs;
+  const u32* key;
+  size_t key_bs;
+  u32* out;                 // batch x 2 x (l+1)
+  size_t out_bs;
+  const u32 *e0, *e1;       // epilogue (MUL: ct1, ct2; ROT: ct)
+  size_t e_bs;
+  u32 g;
+};
+
+template <int L1, int L2>
+static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t s) {
+  using S = NttShape<L1, L2>;
+  const LfKsPlan* P = ctx->ks;
+  const KsLevelPlan& K = P->lv[c.level];
+  const int l1 = c.level + 1, alpha = P->n_special;
+  const size_t N = ctx->N;
+  const KsWs w = carve(ctx, c.level, ws);
+  const LfDev dv = ctx->dev();
+  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const int groups = (1 << L1) / S::LPCR;
+
+  // K_A
+  {
+    const int nlines = l1 << L1;
+    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, c.batch);
+    if (c.op == OP_MUL)
+      k_modup_in<L1, L2, 1><<<grid, S::TR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1);
+    else
+      k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1);
+    LF_CHECK_LAUNCH();
+  }
+  // K_BC (ModUp)
+  {
+    BcArgs A{};
+    A.src = w.T0; A.dst = w.T1; A.src_bs = w.per; A.dst_bs = w.per;
+    A.ngroups = K.beta;
+    int kmax = 0, mmax = 0;
+    for (int j = 0; j < K.beta; ++j) {
+      A.g[j] = K.up[j];
+      kmax = K.up[j].B.k > kmax ? K.up[j].B.k : kmax;
+      mmax = K.up[j].B.m > mmax ? K.up[j].B.m : mmax;
+    }
+    A.tsplit = bc_tsplit(K.beta, c.batch, (1 << L2) / 8, mmax);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, kmax, s)) return e;
+  }
+  // K_C
+  {
+    KsInnerArgs A{};
+    A.T1 = w.T1; A.x = c.x; A.x2 = c.x2; A.key = c.key; A.acc = w.acc; A.T2 = w.T2;
+    A.t1_bs = w.per; A.x_bs = c.x_bs; A.key_bs = c.key_bs; A.acc_bs = w.per; A.t2_bs = w.per;
+    A.rowk = P->rowk; A.level = c.level; A.d = P->d; A.beta = K.beta; A.L = P->L; A.alpha = alpha;
+    A.R = P->L + 1 + alpha; A.g = c.g;
+    const size_t smC = (size_t)S::LPCR * (pitchR<L2>() + LineCfg<L2>::M) * 4;
+    dim3 grid(K.ext * groups, 1, c.batch);
+    if (c.op == OP_ROT) k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv);
+    else if (c.op == OP_MUL) k_ks_inner<L1, L2, false, 1><<<grid, S::TRR, smC, s>>>(A, dv);
+    else k_ks_inner<L1, L2, false, 0><<<grid, S::TRR, smC, s>>>(A, dv);
+    LF_CHECK_LAUNCH();
+  }
+  // K_BC (ModDown)
+  {
+    BcArgs A{};
+    A.src = w.T2; A.dst = w.T3; A.src_bs = w.per; A.dst_bs = w.per;
+    A.ngroups = 2;
+    for (int p = 0; p < 2; ++p) {
+      A.g[p].B = P->down;
+      A.g[p].B.m = l1;                     // prefix of the level-L table
+      A.g[p].src_rows = P->iota;
+      A.g[p].dst_rows = P->iota;
+      A.g[p].src_row0 = p * alpha;
+      A.g[p].dst_row0 = p * l1;
+    }
+    A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, l1);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, alpha, s)) return e;
+  }
+  // K_E
+  {
+    ModDownArgs A{};
+    A.T3 = w.T3; A.acc = w.acc; A.out = c.out; A.e0 = c.e0; A.e1 = c.e1;
+    A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
+    A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1; A.g = c.g;
+    dim3 grid(l1 * groups, 1, c.batch);
+    if (c.op == OP_MUL) k_moddown_out<L1, L2, EPI_MUL><<<grid, S::TRR, smR, s>>>(A, dv);
+    else if (c.op == OP_ROT) k_moddown_out<L1, L2, EPI_ROT><<<grid, S::TRR, smR, s>>>(A, dv);
+    else k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv);
+    LF_CHECK_LAUNCH();
+  }
+  (void)N;
+  return 0;
+}
+
+template <int L1, int L2>
+static int rescale_pipeline(const LfCtx* ctx, int level, const u32* ct, size_t ct_bs, u32* out,
+                            size_t out_bs, int batch, void* ws, cudaStream_t s) {
+  using S = NttShape<L1, L2>;
+  const LfKsPlan* P = ctx->ks;
+  const KsLevelPlan& K = P->lv[level];
+  const int l = level;
+  const size_t N = ctx->N;
+  const LfDev dv = ctx->dev();
+  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const int groups = (1 << L1) / S::LPCR;
+  u32* T2 = (u32*)ws;                      // per instance: 2 rows, then T3: 2 l rows
+  const size_t per = (2 + 2 * (size_t)l) * N;
+  u32* T3 = T2 + 2 * N;
+  {  // row pass of INTT(b_l), INTT(a_l)  (poly.py:284-287 -> mod_down of the top prime)
+    const int nlines = 2 << L1;
+    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, batch);
+    k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2, dv, l + 1, l, l);
+    LF_CHECK_LAUNCH();
+  }
+  {
+    BcArgs A{};
+    A.src = T2; A.dst = T3; A.src_bs = per; A.dst_bs = per;
+    A.ngroups = 2;
+    A.g[0] = K.resc[0];
+    A.g[1] = K.resc[1];
+    A.tsplit = bc_tsplit(2, batch, (1 << L2) / 8, l);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, batch, 1, s)) return e;
+  }
+  {
+    ModDownArgs A{};
+    A.T3 = T3; A.acc = ct; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
+    A.t3_bs = per; A.acc_bs = ct_bs; A.out_bs = out_bs; A.e_bs = 0;
+    A.scal = P->qinv + (size_t)l * P->n_main * 2; A.sstride = 2;
+    A.nt = l; A.nacc = l + 1; A.ne = 0; A.g = 0;
+    dim3 grid(l * groups, 1, batch);
+    k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv);
+    LF_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+template <int L1, int L2>
+static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pieces, void* ws,
+                              cudaStream_t s) {
+  using S = NttShape<L1, L2>;
+  const LfKsPlan* P = ctx->ks;
+  const KsLevelPlan& K = P->lv[level];
+  const int l1 = level + 1;
+  const KsWs w = carve(ctx, level, ws);
+  const LfDev dv = ctx->dev();
+  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const int groups = (1 << L1) / S::LPCR;
+  {
+    const int nlines = l1 << L1;
+    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, 1);
+    k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, 1, 0, -1);
+    LF_CHECK_LAUNCH();
+  }
+  {
+    BcArgs A{};
+    A.src = w.T0; A.dst = w.T1; A.ngroups = K.beta;
+    int kmax = 0, mmax = 0;
+    for (int j = 0; j < K.beta; ++j) {
+      A.g[j] = K.up[j];
+      kmax = K.up[j].B.k > kmax ? K.up[j].B.k : kmax;
+      mmax = K.up[j].B.m > mmax ? K.up[j].B.m : mmax;
+    }
+    A.tsplit = bc_tsplit(K.beta, 1, (1 << L2) / 8, mmax);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, 1, kmax, s)) return e;
+  }
+  {
+    dim3 grid(K.beta * K.ext * groups);
+    k_pieces<L1, L2><<<grid, S::TRR, smR, s>>>(w.T1, x, pieces, P->rowk, level, P->d, P->L,
+                                              P->n_special, dv);
+    LF_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+// =======================================================================================
+// C ABI
+static int ks_check(const lf_ctx* ctx, int level) {
+  if (!ctx) { lf_set_error("null context"); return 1; }
+  if (!ctx->ks) { lf_set_error("keyswitch plans not built (call lf_ctx_enable_keyswitch)"); return 2; }
+  if (level < 0 || level > ctx->ks->L) { lf_set_error("level %d outside [0, %d]", level, ctx->ks->L); return 2; }
+  return 0;
+}
+
+static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s) {
+#define LF_KS(A, B) { if (int e = ks_pipeline<A, B>(ctx, c, ws, s)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_KS)
+#undef LF_KS
+  return 0;
+}
+
+extern "C" {
+
+int lf_ctx_enable_keyswitch(lf_ctx* ctx, int n_main, int d) {
+  if (!ctx) { lf_set_error("null context"); return 1; }
+  return lf_build_ks_plan(ctx, n_main, d);
+}
+
+size_t lf_ks_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
+  if (ks_check(ctx, level)) return 0;
+  return ks_ws_rows(ctx->ks, level) * (size_t)ctx->N * 4 * (size_t)(batch < 1 ? 1 : batch);
+}
+
+int lf_keyswitch(const lf_ctx* ctx, int level, const uint32_t* x, size_t x_bstride,
+                 const uint32_t* evk, size_t evk_bstride, uint32_t* out, size_t out_bstride,
+                 int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!x || !evk || !out || !workspace) { lf_set_error("lf_keyswitch: null argument"); return 1; }
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_KS;
+  c.x = x; c.x2 = x; c.x_bs = x_bstride; c.key = evk; c.key_bs = evk_bstride;
+  c.out = out; c.out_bs = out_bstride;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t* ct2,
+               size_t ct_bstride, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
+               int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct1 || !ct2 || !rlk || !out || !workspace) { lf_set_error("lf_hom_mul: null argument"); return 1; }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_MUL;
+  c.x = ct1 + arow; c.x2 = ct2 + arow; c.x_bs = ct_bstride; c.key = rlk; c.key_bs = 0;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct_bstride;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_rotate(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride, uint32_t g,
+              const uint32_t* key, size_t key_bstride, uint32_t* out, size_t out_bstride,
+              int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct || !key || !out || !workspace) { lf_set_error("lf_rotate: null argument"); return 1; }
+  if (!(g & 1)) { lf_set_error("lf_rotate: galois element must be odd"); return 2; }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_ROT;
+  c.x = ct + arow; c.x2 = c.x; c.x_bs = ct_bstride; c.key = key; c.key_bs = key_bstride;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct; c.e1 = nullptr; c.e_bs = ct_bstride;
+  c.g = g & ((2u << ctx->logN) - 1);
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
+  if (!ctx) return 0;
+  return (2 + 2 * (size_t)level) * ctx->N * 4 * (size_t)(batch < 1 ? 1 : batch);
+}
+
+int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,
+               uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (level < 1) { lf_set_error("rescale at level 0"); return 2; }
+  if (!ct || !out || !workspace) { lf_set_error("lf_rescale: null argument"); return 1; }
+#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_RS)
+#undef LF_RS
+  return 0;
+}
+
+int lf_ks_decompose(const lf_ctx* ctx, int level, const uint32_t* x, uint32_t* pieces,
+                    void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!x || !pieces || !workspace) { lf_set_error("lf_ks_decompose: null argument"); return 1; }
+#define LF_DC(A, B) { if (int e = decompose_pipeline<A, B>(ctx, level, x, pieces, workspace, (cudaStream_t)stream)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_DC)
+#undef LF_DC
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// Register-resident NTT line transforms.
+//
+// A row of N = 2^L residues is viewed as a 2^L1 x 2^L2 matrix, element e = hi*2^L2 + lo.
+// The reference's forward transform (ntt.py:70-86) is a Cooley-Tukey network whose stage s
+// pairs elements at distance N/2^(s+1) with twiddle psi_brv[2^s + (e >> (L-s))].  The first
+// L1 stages only mix `hi` (one independent 2^L1-point "column line" per lo) and the last L2
+// stages only mix `lo` (one "row line" per hi).  In both cases stage k of a line uses twiddle
+// index (R << k) + (p >> (LP - k)) where p is the position inside the line and R the line's
+// root in the heap-ordered twiddle table: R = 1 for column lines, R = 2^L1 + hi for row lines.
+// The inverse (ntt.py:89-105) is the Gentleman-Sande network with the same indexing.
+//
+// A line of LP stages (M = 2^LP points) is processed by T = 2^floor(LP/2) threads each
+// holding E = 2^ceil(LP/2) registers:
+//   step 1: thread tl holds positions p = tl + T*j (j < E); runs the first LA = ceil(LP/2)
+//           stages entirely in registers (root R).
+//   exchange through shared memory.
+//   step 2: thread tl holds positions p = tl*E + e (e < E), i.e. G = E/T contiguous groups of
+//           T points, each an independent LB = floor(LP/2)-stage sub-transform with root
+//           (R << LA) + tl*G + gi.
+// Forward: step1 -> exchange -> step2.  Inverse: step2^-1 -> exchange -> step1^-1.
+//
+// Lazy reduction (forward): a butterfly outputs X + T and X - T + 2q with T = Shoup(Y) in
+// [0, 2q), so the bound grows by 2q per stage and only X needs an occasional csub(8q) to stay
+// below 16q < 2^32.  The bound is tracked at compile time (units of q).  The inverse uses
+// Harvey's butterfly with inputs/outputs in [0, 2q).
+#pragma once
+#include "lf_arith.cuh"
+
+template <int LP>
+struct LineCfg {
+  static constexpr int LA = (LP + 1) / 2;
+  static constexpr int LB = LP / 2;
+  static constexpr int T = 1 << LB;
+  static constexpr int E = 1 << LA;
+  static constexpr int G = E / T;
+  static constexpr int M = 1 << LP;
+};
+
+// ---- compile-time bound tracking for the lazy forward butterflies ------------------------
+__host__ __device__ constexpr bool fwd_needs_corr(int b) { return b + 2 > 16; }
+__host__ __device__ constexpr int fwd_next_bound(int b) { return (fwd_needs_corr(b) ? 8 : b) + 2; }
+__host__ __device__ constexpr int fwd_bound_at(int b, int stages) {
+  return stages == 0 ? b : fwd_bound_at(fwd_next_bound(b), stages - 1);
+}
+
+// Forward CT sub-transform of 2^K registers.  Input bound BIN (units of q).
+template <int K, int BIN>
+LF_DEV void ct_sub(u32* x, u32 root, const uint2* __restrict__ tw, u32 q) {
+  static_assert(BIN <= 16, "input bound too large");
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int h = 1 << (K - 1 - k);
+    const bool corr = fwd_needs_corr(fwd_bound_at(BIN, k));
+#pragma unroll
+    for (int blk = 0; blk < (1 << k); ++blk) {
+      const uint2 w = __ldg(&tw[(root << k) + blk]);
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        u32 X = x[blk * 2 * h + j];
+        const u32 Y = x[blk * 2 * h + h + j];
+        if (corr) X = csub(X, 8 * q);
+        const u32 t = mul_shoup_lazy(Y, w.x, w.y, q);
+        x[blk * 2 * h + j] = X + t;
+        x[blk * 2 * h + h + j] = X - t + 2 * q;
+      }
+    }
+  }
+}
+
+// Inverse GS sub-transform of 2^K registers, Harvey butterflies, [0,2q) in and out.
+template <int K>
+LF_DEV void gs_sub(u32* x, u32 root, const uint2* __restrict__ tw, u32 q) {
+#pragma unroll
+  for (int k = K - 1; k >= 0; --k) {
+    const int h = 1 << (K - 1 - k);
+#pragma unroll
+    for (int blk = 0; blk < (1 << k); ++blk) {
+      const uint2 w = __ldg(&tw[(root << k) + blk]);
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const u32 X = x[blk * 2 * h + j];
+        const u32 Y = x[blk * 2 * h + h + j];
+        x[blk * 2 * h + j] = csub(X + Y, 2 * q);
+        x[blk * 2 * h + h + j] = mul_shoup_lazy(X - Y + 2 * q, w.x, w.y, q);
+      }
+    }
+  }
+}
+
+// Output bound (units of q) of a full forward line with input bound BIN.
+template <int LP, int BIN>
+struct FwdLineBound {
+  static constexpr int step1 = fwd_bound_at(BIN, LineCfg<LP>::LA);
+  static constexpr int value = fwd_bound_at(step1, LineCfg<LP>::LB);
+};
+
+// Exchange helpers.  `Addr` maps a line position to a shared-memory word index for the
+// calling thread's line.  Sync is the barrier covering all threads of a line.
+template <int LP, class Addr, class Sync>
+LF_DEV void xchg_12(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
+  using C = LineCfg<LP>;
+#pragma unroll
+  for (int j = 0; j < C::E; ++j) sm[addr(tl + C::T * j)] = x[j];
+  sync();
+#pragma unroll
+  for (int e = 0; e < C::E; ++e) x[e] = sm[addr(tl * C::E + e)];
+}
+
+template <int LP, class Addr, class Sync>
+LF_DEV void xchg_21(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
+  using C = LineCfg<LP>;
+#pragma unroll
+  for (int e = 0; e < C::E; ++e) sm[addr(tl * C::E + e)] = x[e];
+  sync();
+#pragma unroll
+  for (int j = 0; j < C::E; ++j) x[j] = sm[addr(tl + C::T * j)];
+}
+
+// Forward line: x in step-1 layout (bound BIN) -> step-2 layout (bound FwdLineBound).
+// The caller must make sure `sm` is free to overwrite (pre-sync) when needed.
+template <int LP, int BIN, class Addr, class Sync>
+LF_DEV void fwd_line(u32* x, u32 root, const uint2* __restrict__ tw, u32 q, u32* sm, int tl,
+                     Addr addr, Sync sync) {
+  using C = LineCfg<LP>;
+  ct_sub<C::LA, BIN>(x, root, tw, q);
+  xchg_12<LP>(x, sm, tl, addr, sync);
+  constexpr int B1 = FwdLineBound<LP, BIN>::step1;
+#pragma unroll
+  for (int gi = 0; gi < C::G; ++gi)
+    ct_sub<C::LB, B1>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
+}
+
+// Inverse line: x in step-2 layout ([0,2q)) -> step-1 layout ([0,2q)), no N^-1 scaling.
+template <int LP, class Addr, class Sync>
+LF_DEV void inv_line(u32* x, u32 root, const uint2* __restrict__ tw, u32 q, u32* sm, int tl,
+                     Addr addr, Sync sync) {
+  using C = LineCfg<LP>;
+#pragma unroll
+  for (int gi = 0; gi < C::G; ++gi)
+    gs_sub<C::LB>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
+  xchg_21<LP>(x, sm, tl, addr, sync);
+  gs_sub<C::LA>(x, root, tw, q);
+}

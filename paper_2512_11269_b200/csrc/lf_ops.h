@@ -1,0 +1,11 @@
+// Internal launcher declarations (not part of the public ABI).
+#pragma once
+#include "lf_b200.h"
+#include "lf_common.cuh"
+
+int lf_launch_ewise(const LfCtx* ctx, int op, u32* out, const u32* a, const u32* b,
+                    const u32* c, const RowMap& rm, const u32* scalars, cudaStream_t s);
+int lf_launch_automorph(const LfCtx* ctx, u32* out, const u32* in, u32 g, int nrows,
+                        cudaStream_t s);
+int lf_launch_bconv(const LfCtx* ctx, u32* out, const u32* src, const u32* tab, int k, int m,
+                    int W, cudaStream_t s);

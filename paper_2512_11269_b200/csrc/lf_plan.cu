@@ -1,0 +1,258 @@
+// Host construction of the keyswitch / rescale plans (constants of reference ckks.py:85-140,
+// poly.py:140-178, 251-287, keys.py:85-97), uploaded to HBM in one allocation.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "lf_plan.h"
+
+namespace {
+
+typedef std::vector<u32> Big;   // little-endian 32-bit words
+
+u32 mulm(u32 a, u32 b, u32 q) { return (u32)((u64)a * b % q); }
+u32 powm(u32 b, u64 e, u32 q) {
+  u64 r = 1, x = b % q;
+  while (e) {
+    if (e & 1) r = r * x % q;
+    x = x * x % q;
+    e >>= 1;
+  }
+  return (u32)r;
+}
+u32 invm(u32 a, u32 q) { return powm(a, q - 2, q); }
+u32 shoupc(u32 w, u32 q) { return (u32)(((u64)w << 32) / q); }
+
+void big_mul(Big& a, u32 m) {
+  u64 carry = 0;
+  for (auto& w : a) {
+    u64 t = (u64)w * m + carry;
+    w = (u32)t;
+    carry = t >> 32;
+  }
+  if (carry) a.push_back((u32)carry);
+}
+
+struct Blob {
+  std::vector<u32> w;
+  size_t align2() {            // keep doubles 8-byte aligned
+    if (w.size() & 1) w.push_back(0);
+    return w.size();
+  }
+  size_t push(const std::vector<u32>& v) {
+    size_t o = w.size();
+    w.insert(w.end(), v.begin(), v.end());
+    return o;
+  }
+};
+
+struct TabRec {
+  size_t off;
+  int k, m, W;
+};
+
+// Exact base-conversion table (layout lf_bconv_view).  `mult[i]` is folded into c_i.
+TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<int>& src,
+                   const std::vector<int>& tgt, const std::vector<u32>& mult) {
+  const int k = (int)src.size(), m = (int)tgt.size();
+  Big S{1};
+  for (int i : src) big_mul(S, primes[i]);
+  while (S.size() > 1 && S.back() == 0) S.pop_back();
+  const int W = (int)S.size() + 1;
+  TabRec r{b.align2(), k, m, W};
+  std::vector<u32> v;
+  for (int i = 0; i < k; ++i) {
+    double inv = 1.0 / (double)primes[src[i]];
+    u32 two[2];
+    memcpy(two, &inv, 8);
+    v.push_back(two[0]);
+    v.push_back(two[1]);
+  }
+  for (int i = 0; i < k; ++i) v.push_back((u32)src[i]);
+  std::vector<u32> c(k);
+  for (int i = 0; i < k; ++i) {
+    const u32 s = primes[src[i]];
+    u32 hat = 1;                                   // (S/s_i) mod s_i
+    for (int j = 0; j < k; ++j)
+      if (j != i) hat = mulm(hat, primes[src[j]] % s, s);
+    c[i] = mulm(invm(hat, s), mult[i] % s, s);
+  }
+  for (int i = 0; i < k; ++i) v.push_back(c[i]);
+  for (int i = 0; i < k; ++i) v.push_back(shoupc(c[i], primes[src[i]]));
+  for (int t = 0; t < m; ++t) v.push_back((u32)tgt[t]);
+  for (int t = 0; t < m; ++t) {
+    const u32 q = primes[tgt[t]];
+    u32 sm = 1;
+    for (int i = 0; i < k; ++i) sm = mulm(sm, primes[src[i]] % q, q);
+    v.push_back((q - sm) % q);
+  }
+  for (int t = 0; t < m; ++t) {
+    const u32 q = primes[tgt[t]];
+    for (int i = 0; i < k; ++i) {
+      u32 h = 1;
+      for (int j = 0; j < k; ++j)
+        if (j != i) h = mulm(h, primes[src[j]] % q, q);
+      v.push_back(h);
+    }
+  }
+  for (int i = 0; i < k; ++i) {
+    Big h{1};
+    for (int j = 0; j < k; ++j)
+      if (j != i) big_mul(h, primes[src[j]]);
+    h.resize(W, 0);
+    v.insert(v.end(), h.begin(), h.end());
+  }
+  Big Sw = S;
+  Sw.resize(W, 0);
+  v.insert(v.end(), Sw.begin(), Sw.end());
+  b.push(v);
+  return r;
+}
+
+}  // namespace
+
+int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
+  const int n_sp = ctx->nprimes - n_main;
+  if (n_main < 2 || n_main > LF_MAXMAIN || n_sp < 1 || d < 1 || d > LF_MAXD) {
+    lf_set_error("keyswitch plan: n_main=%d n_special=%d d=%d outside limits", n_main, n_sp, d);
+    return 2;
+  }
+  if (n_sp > 64) { lf_set_error("keyswitch plan: too many special primes"); return 2; }
+  const int L = n_main - 1;
+  std::vector<u32> primes(ctx->nprimes), ninv(ctx->nprimes);
+  for (int i = 0; i < ctx->nprimes; ++i) {
+    primes[i] = ctx->h_pk[i].q;
+    ninv[i] = ctx->h_pk[i].ninv;
+  }
+  Blob blob;
+  // identity row list
+  std::vector<u32> iota(n_main > n_sp ? n_main : n_sp);
+  for (size_t i = 0; i < iota.size(); ++i) iota[i] = (u32)i;
+  const size_t off_iota = blob.push(iota);
+
+  // decomposition scalars s_i for the own digit of limb i: (Q_L/Q_Dj mod q_i)^-1, j = i % d
+  // (ckks.py:85-92, keys.py:85-92), and P^-1 mod q_i (poly.py:280)
+  auto dec_scalar = [&](int j, int i) {
+    const u32 q = primes[i];
+    u32 f = 1;
+    for (int t = 0; t <= L; ++t)
+      if (t % d != j) f = mulm(f, primes[t] % q, q);
+    return invm(f, q);
+  };
+  std::vector<u32> rowk;
+  for (int t = 0; t <= L; ++t) {
+    const u32 q = primes[t];
+    const u32 s = dec_scalar(t % d, t);
+    u32 P = 1;
+    for (int j = 0; j < n_sp; ++j) P = mulm(P, primes[n_main + j] % q, q);
+    const u32 pinv = invm(P, q);
+    rowk.insert(rowk.end(), {s, shoupc(s, q), pinv, shoupc(pinv, q)});
+  }
+  const size_t off_rowk = blob.push(rowk);
+  std::vector<u32> qinv((size_t)n_main * n_main * 2, 0);
+  for (int l = 1; l <= L; ++l)
+    for (int t = 0; t < l; ++t) {
+      const u32 q = primes[t], v = invm(primes[l] % q, q);
+      qinv[((size_t)l * n_main + t) * 2] = v;
+      qinv[((size_t)l * n_main + t) * 2 + 1] = shoupc(v, q);
+    }
+  const size_t off_qinv = blob.push(qinv);
+
+  // ModDown table: specials -> main 0..L, y-multiplier folds the INTT's N^-1.
+  std::vector<int> sp_src, main_all;
+  std::vector<u32> sp_mult;
+  for (int j = 0; j < n_sp; ++j) { sp_src.push_back(n_main + j); sp_mult.push_back(ninv[n_main + j]); }
+  for (int t = 0; t <= L; ++t) main_all.push_back(t);
+  const TabRec down = build_table(blob, primes, sp_src, main_all, sp_mult);
+
+  // per level
+  struct LvRec {
+    int beta, ext;
+    TabRec up[LF_MAXD];
+    size_t src_off[LF_MAXD], dst_off[LF_MAXD];
+    TabRec resc;
+  };
+  std::vector<LvRec> lvr(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    LvRec& R = lvr[l];
+    const int ext = l + 1 + n_sp;
+    R.ext = ext;
+    R.beta = d < l + 1 ? d : l + 1;
+    for (int j = 0; j < R.beta; ++j) {
+      std::vector<int> src, tgt;
+      std::vector<u32> mult, srows, drows;
+      for (int i = j; i <= l; i += d) {
+        src.push_back(i);
+        mult.push_back(mulm(ninv[i], dec_scalar(j, i), primes[i]));
+        srows.push_back((u32)i);
+      }
+      for (int pos = 0; pos < ext; ++pos) {
+        const int pi = pos <= l ? pos : n_main + (pos - l - 1);
+        if (pos <= l && pos % d == j) continue;
+        tgt.push_back(pi);
+        drows.push_back((u32)pos);
+      }
+      R.up[j] = build_table(blob, primes, src, tgt, mult);
+      R.src_off[j] = blob.push(srows);
+      R.dst_off[j] = blob.push(drows);
+    }
+    if (l >= 1) {
+      std::vector<int> src{l}, tgt;
+      for (int t = 0; t < l; ++t) tgt.push_back(t);
+      R.resc = build_table(blob, primes, src, tgt, {ninv[l]});
+    }
+  }
+
+  void* dmem = nullptr;
+  if (cudaMalloc(&dmem, blob.w.size() * 4) != cudaSuccess ||
+      cudaMemcpy(dmem, blob.w.data(), blob.w.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    lf_set_error("keyswitch plan: device allocation failed");
+    return 3;
+  }
+  const u32* base = (const u32*)dmem;
+  auto view = [&](const TabRec& r) { return lf_bconv_view(base + r.off, r.k, r.m, r.W); };
+
+  LfKsPlan* P = new LfKsPlan();
+  P->n_main = n_main;
+  P->n_special = n_sp;
+  P->d = d;
+  P->L = L;
+  P->dmem = dmem;
+  P->iota = (const int*)(base + off_iota);
+  P->rowk = base + off_rowk;
+  P->qinv = base + off_qinv;
+  P->down = view(down);
+  P->lv.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    KsLevelPlan& K = P->lv[l];
+    const LvRec& R = lvr[l];
+    K.level = l;
+    K.beta = R.beta;
+    K.ext = R.ext;
+    for (int j = 0; j < R.beta; ++j) {
+      K.up[j].B = view(R.up[j]);
+      K.up[j].src_rows = (const int*)(base + R.src_off[j]);
+      K.up[j].dst_rows = (const int*)(base + R.dst_off[j]);
+      K.up[j].src_row0 = 0;
+      K.up[j].dst_row0 = j * R.ext;
+    }
+    if (l >= 1) {
+      for (int p = 0; p < 2; ++p) {
+        K.resc[p].B = view(R.resc);
+        K.resc[p].src_rows = P->iota;
+        K.resc[p].dst_rows = P->iota;
+        K.resc[p].src_row0 = p;
+        K.resc[p].dst_row0 = p * l;
+      }
+    }
+  }
+  if (ctx->ks) lf_free_ks_plan(ctx->ks);
+  ctx->ks = P;
+  return 0;
+}
+
+void lf_free_ks_plan(LfKsPlan* p) {
+  if (!p) return;
+  cudaFree(p->dmem);
+  delete p;
+}

@@ -1,0 +1,38 @@
+// Keyswitch / rescale plans: every constant the fused kernels need, built once per context on
+// the host from the prime list (no big-integer library: products are formed word by word) and
+// kept resident in HBM.
+#pragma once
+#include <vector>
+
+#include "lf_bconv.cuh"
+
+#define LF_MAXD 16        // max digits d
+#define LF_MAXMAIN 64     // max main primes L+1
+
+// One base-conversion group of a K_BC launch: source rows src_row0 + src_rows[i] of the
+// source buffer, target rows dst_row0 + dst_rows[t] of the destination buffer.
+struct BcGroupDev {
+  BconvDev B;
+  const int* src_rows;
+  const int* dst_rows;
+  int src_row0, dst_row0;
+};
+
+struct KsLevelPlan {
+  int level, beta, ext;
+  BcGroupDev up[LF_MAXD];      // ModUp conversion of digit j (sources G_j, targets ext \ G_j)
+  BcGroupDev resc[2];          // rescale at this level: q_level -> q_0..q_{level-1} (b and a)
+};
+
+struct LfKsPlan {
+  int n_main, n_special, d, L;
+  std::vector<KsLevelPlan> lv;     // index = level
+  BconvDev down;                   // ModDown: specials -> main 0..L (prefix per level)
+  const int* iota;                 // device 0..max(n_main, n_special) identity row list
+  const u32* rowk;                 // [n_main][4]: s_t, s_t' (own-digit decomposition scalar), P^-1, P^-1'
+  const u32* qinv;                 // [n_main][n_main][2]: q_l^-1 mod q_t and Shoup companion
+  void* dmem;
+};
+
+int lf_build_ks_plan(struct LfCtx* ctx, int n_main, int d);
+void lf_free_ks_plan(LfKsPlan* p);

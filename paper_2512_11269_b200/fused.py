@@ -1,0 +1,101 @@
+"""Host side of the fused keyswitch pipeline (csrc/lf_ks.cu via the C ABI).
+
+Ciphertexts are handed to the kernels as one (2, level+1, N) block (b rows then a rows,
+include/lf_b200.h); results come back the same way and are exposed as two views, so chained
+operations never copy.
+"""
+
+import torch
+
+from . import _native
+from .context import dptr, get_context, stream_handle
+from .poly import Domain, RnsPolynomial, extended_ids, main_ids
+
+
+def ct_block(ct) -> torch.Tensor:
+    """(2, l+1, N) view of a ciphertext's residues; stacks only if b and a are not adjacent."""
+    b, a = ct.b.limbs, ct.a.limbs
+    n = b.numel()
+    if (b.is_contiguous() and a.is_contiguous() and a.data_ptr() == b.data_ptr() + 4 * n
+            and a.untyped_storage().data_ptr() == b.untyped_storage().data_ptr()):
+        return b.as_strided((2, *b.shape), (n, b.shape[1], 1), b.storage_offset())
+    return torch.stack([b, a])
+
+
+def _pair(out: torch.Tensor, ids):
+    return (RnsPolynomial(out[0], Domain.EVAL, ids), RnsPolynomial(out[1], Domain.EVAL, ids))
+
+
+def keyswitch(params, x: RnsPolynomial, evk):
+    ctx = get_context(params)
+    level = len(x.basis_ids) - 1
+    ws = ctx.ks_workspace(level)
+    out = torch.empty((2, level + 1, params.N), dtype=torch.int32, device=x.limbs.device)
+    xl = x.limbs.contiguous()
+    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xl), 0, dptr(evk.data), 0,
+                                             dptr(out), 0, 1, dptr(ws), stream_handle()),
+                  "lf_keyswitch")
+    return _pair(out, main_ids(level))
+
+
+def hom_mul(params, ct1, ct2, rlk):
+    ctx = get_context(params)
+    level = ct1.level
+    ws = ctx.ks_workspace(level)
+    c1, c2 = ct_block(ct1), ct_block(ct2)
+    out = torch.empty_like(c1)
+    _native.check(_native.lib().lf_hom_mul(ctx.handle, level, dptr(c1), dptr(c2), 0, dptr(rlk.data),
+                                           dptr(out), 0, 1, dptr(ws), stream_handle()), "lf_hom_mul")
+    return _pair(out, main_ids(level))
+
+
+def rotate(params, ct, g: int, key):
+    ctx = get_context(params)
+    level = ct.level
+    ws = ctx.ks_workspace(level)
+    c = ct_block(ct)
+    out = torch.empty_like(c)
+    _native.check(_native.lib().lf_rotate(ctx.handle, level, dptr(c), 0, g, dptr(key.data), 0,
+                                          dptr(out), 0, 1, dptr(ws), stream_handle()), "lf_rotate")
+    return _pair(out, main_ids(level))
+
+
+def rescale(params, ct):
+    ctx = get_context(params)
+    level = ct.level
+    ws = ctx.rescale_workspace(level)
+    c = ct_block(ct)
+    out = torch.empty((2, level, params.N), dtype=torch.int32, device=c.device)
+    _native.check(_native.lib().lf_rescale(ctx.handle, level, dptr(c), 0, dptr(out), 0, 1, dptr(ws),
+                                           stream_handle()), "lf_rescale")
+    return _pair(out, main_ids(level - 1))
+
+
+def decompose(params, x: RnsPolynomial):
+    ctx = get_context(params)
+    level = len(x.basis_ids) - 1
+    ext = extended_ids(params, level)
+    beta = min(params.ks.d, level + 1)
+    ws = ctx.ks_workspace(level)
+    pieces = torch.empty((beta, len(ext), params.N), dtype=torch.int32, device=x.limbs.device)
+    xl = x.limbs.contiguous()
+    _native.check(_native.lib().lf_ks_decompose(ctx.handle, level, dptr(xl), dptr(pieces), dptr(ws),
+                                                stream_handle()), "lf_ks_decompose")
+    return [(j, RnsPolynomial(pieces[j], Domain.EVAL, ext)) for j in range(beta)]
+
+
+# --- batched entry points (bench / bootstrap) -------------------------------------------
+
+def keyswitch_batch(params, level: int, xs: torch.Tensor, evk, out: torch.Tensor = None,
+                    ws: torch.Tensor = None):
+    """xs: (B, level+1, N) -> out (B, 2, level+1, N); one shared key."""
+    ctx = get_context(params)
+    B = xs.shape[0]
+    if ws is None:
+        ws = ctx.ks_workspace(level, B)
+    if out is None:
+        out = torch.empty((B, 2, level + 1, params.N), dtype=torch.int32, device=xs.device)
+    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xs), xs[0].numel(), dptr(evk.data), 0,
+                                             dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
+                  "lf_keyswitch")
+    return out
