@@ -1,0 +1,373 @@
+"""Benchmark: full-level hybrid keyswitch throughput at N=2^16 (BASELINE config 2 / SURVEY
+§8(d) C2: gen_params(65536, 35, d=4, seed=0, scale=2^26) -> 36 main + 9 special primes,
+4 digits, ext = 45 rows).
+
+One step = one batch of B independent full-level keyswitches (relinearisation of B
+ciphertexts, one shared relinearisation key), inputs resident in HBM.  `value` is keyswitch
+ops/s over the whole job (all ranks); `e2e` is the same metric through the public operator
+API (`paper_2512_11269_b200.keyswitch`) with the inputs copied from pinned host memory and
+the results copied back inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+`--impl reference` times the reference algorithm on the host CPU cores instead (the CPU
+oracle `oracle/lf_oracle.py`, a restatement of limbforge ckks.keyswitch — the reference
+itself is pure Python and cannot travel to the GPU box), with one worker process per core.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(N=65536, num_levels=35, d=4, seed=0, scale=2 ** 26)
+ROW_BYTES = 65536 * 4
+METRIC = "keyswitch ops/s"
+STAGES = ["modup_in", "modup_bconv", "ks_inner", "moddown_bconv", "moddown_out"]
+
+
+def algorithmic_rows(level=35, d=4, alpha=9):
+    """keyswitch(x) = (l+1) + 2*beta*ext + 2(l+1) rows of N uint32 words."""
+    l1 = level + 1
+    beta = min(d, l1)
+    ext = l1 + alpha
+    return l1 + 2 * beta * ext + 2 * l1
+
+
+def stage_rows(level=35, d=4, alpha=9):
+    """Algorithmic rows read+written by each fused kernel ('Kernels')."""
+    l1 = level + 1
+    beta = min(d, l1)
+    ext = l1 + alpha
+    conv_rows = beta * ext - l1          # piece rows produced by base conversion
+    return {
+        "modup_in": l1 + l1,                                   # x in, T0 out
+        "modup_bconv": l1 + conv_rows,                         # T0 in, T1 out
+        "ks_inner": conv_rows + l1 + 2 * beta * ext + 2 * l1 + 2 * alpha,   # T1, x, keys in; acc, T2 out
+        "moddown_bconv": 2 * alpha + 2 * l1,                   # T2 in, T3 out
+        "moddown_out": 2 * l1 + 2 * l1 + 2 * l1,               # T3, acc in; out
+    }
+
+
+# ----------------------------------------------------------------------------------------
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event (throttle) reasons during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, torch_device_index, period_s=0.001):
+        import threading
+        self.period = period_s
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            props = torch.cuda.get_device_properties(torch_device_index)
+            try:
+                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._thread = threading.Thread(target=self._run, daemon=True)
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self._thread:
+            self._thread.start()
+        return self
+
+    def stop(self):
+        if not self._thread:
+            return None
+        self._stop.set()
+        self._thread.join()
+        if not self.samples:
+            try:
+                self._sample()
+            except Exception:
+                return None
+        names = sorted(n for n, bit in self.REASONS.items() if self.reasons & bit)
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------------
+def cpu_oracle_keyswitch_sample(n_ops=2, level=35):
+    """Time the CPU oracle (restatement of limbforge ckks.keyswitch) on a bounded sample."""
+    from oracle import lf_oracle as O
+    P = O.gen_params(**C2)
+    ext = P.ext_ids(P.L)
+    rng = np.random.default_rng(7)
+    evk = O.EvalKeyO("relin", [(O.sample_uniform(P, rng, ext), O.sample_uniform(P, rng, ext))
+                               for _ in range(P.d)])
+    ids = P.main_ids(level)
+    xs = [O.sample_uniform(P, np.random.default_rng(1000 + i), ids) for i in range(n_ops)]
+    O.twiddles(P.N, P.main[0])  # table build is setup, not timed
+    for q in P.main + P.special:
+        O.twiddles(P.N, q)
+    t0 = time.perf_counter()
+    for x in xs:
+        O.keyswitch(P, x, evk)
+    dt = time.perf_counter() - t0
+    return n_ops / dt, dt
+
+
+_REF_STATE = {}
+
+
+def _ref_worker_init():
+    from oracle import lf_oracle as O
+    P = O.gen_params(**C2)
+    ext = P.ext_ids(P.L)
+    rng = np.random.default_rng(7)
+    evk = O.EvalKeyO("relin", [(O.sample_uniform(P, rng, ext), O.sample_uniform(P, rng, ext))
+                               for _ in range(P.d)])
+    for q in P.main + P.special:
+        O.twiddles(P.N, q)
+    _REF_STATE.update(P=P, evk=evk, O=O)
+
+
+def _ref_worker_ks(seed):
+    O, P, evk = _REF_STATE["O"], _REF_STATE["P"], _REF_STATE["evk"]
+    x = O.sample_uniform(P, np.random.default_rng(seed), P.main_ids(P.L))
+    t0 = time.perf_counter()
+    O.keyswitch(P, x, evk)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (CPU oracle) on all host cores.  The key and
+    twiddle tables are built once in the parent and shared copy-on-write with the workers."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = min(os.cpu_count() or 1, 64)
+    _ref_worker_init()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for w in range(args.warmup):
+            pool.map(_ref_worker_ks, range(cores))
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            pool.map(_ref_worker_ks, [10_000 + k * cores + i for i in range(cores)])
+        dt = time.perf_counter() - t0
+    ops = args.steps * cores
+    value = ops / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ops/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "C2 full-level hybrid keyswitch, N=2^16, L=35, dnum=4, alpha=9",
+                   "level": 35, "batch_per_step": cores, "sample": "one keyswitch per core per step"},
+        "cpu_baseline": {"value": value, "unit": "ops/s", "cores": cores, "kind": "port",
+                         "sample": f"{ops} C2 keyswitches, {cores} worker processes (oracle/lf_oracle.py)"},
+        "e2e": {"value": value, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.context import get_context
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    params = B.gen_params(**C2)
+    level = args.level
+    l1 = level + 1
+    N = params.N
+    sk, pk, rlk = B.keygen(params, seed=11)
+    ctx = get_context(params)
+    Bsz = args.batch
+
+    # synthetic full-level inputs: NSETS distinct batches, cycled (each batch > L2 with keys/outputs)
+    nsets = 3
+    q = torch.tensor(params.rns_basis[:l1], dtype=torch.int64, device=dev)[:, None]
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    xs = []
+    for s in range(nsets):
+        r = torch.randint(0, 2 ** 62, (Bsz, l1, N), device=dev, generator=g, dtype=torch.int64)
+        xs.append((r % q).to(torch.int32))
+    out = torch.empty((Bsz, 2, l1, N), dtype=torch.int32, device=dev)
+    ws = ctx.ks_workspace(level, Bsz)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        fused.keyswitch_batch(params, level, xs[i % nsets], rlk, out=out, ws=ws)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(torch.cuda.current_device()).start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i)                                  # L2 flush between timed steps (untimed)
+        evs[i][0].record(stream)
+        step(i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    total_ops = Bsz * args.steps * world
+    value = total_ops / (ms / 1e3)
+
+    # per-kernel durations (CUDA events on the launch stream), averaged over 3 profiled runs
+    stage = np.zeros(5)
+    for i in range(3):
+        flush.fill_(i)
+        stage += np.array(fused.keyswitch_batch_profiled(params, level, xs[i % nsets], rlk, out, ws))
+    stage /= 3
+    rows = stage_rows(level)
+    stage_info = {n: {"ms": float(t), "share": float(t / stage.sum()),
+                      "gbs": rows[n] * ROW_BYTES * Bsz / (t / 1e3) / 1e9} for n, t in zip(STAGES, stage)}
+    top = max(STAGES, key=lambda n: stage_info[n]["ms"])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    ks_bytes = algorithmic_rows(level) * ROW_BYTES
+    achieved_top = stage_info[top]["gbs"]
+
+    # e2e: public API, pinned host inputs -> device -> keyswitch -> host, every step
+    host_in = torch.empty((Bsz, l1, N), dtype=torch.int32, pin_memory=True)
+    host_in.copy_(xs[0].cpu())
+    host_out = torch.empty((Bsz, 2, l1, N), dtype=torch.int32, pin_memory=True)
+    dev_in = torch.empty((Bsz, l1, N), dtype=torch.int32, device=dev)
+    ids = tuple(range(l1))
+
+    def e2e_step():
+        dev_in.copy_(host_in, non_blocking=True)
+        for b in range(Bsz):
+            kb, ka = B.keyswitch(B.RnsPolynomial(dev_in[b], B.Domain.EVAL, ids), rlk, params)
+            host_out[b, 0].copy_(kb.limbs, non_blocking=True)
+            host_out[b, 1].copy_(ka.limbs, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3
+    e2e_ms = max(e0.elapsed_time(e1), wall_ms)
+    e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+    e2e_value = total_ops / (float(e_t.item()) / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt = cpu_oracle_keyswitch_sample(2, level)
+        cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "port",
+               "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "C2 full-level hybrid keyswitch, N=2^16, L=35, dnum=4, alpha=9",
+                       "level": level, "batch_per_step": Bsz, "parallelism": f"replicas{world}",
+                       "l2": "256 MB flush between timed steps; inputs cycled over 3 batches"},
+            "keyswitch_us": ms / args.steps / Bsz * 1e3,
+            "keyswitch_hbm": {"algorithmic_bytes": ks_bytes, "achieved_gbs": ks_bytes * value / world / 1e9,
+                              "peak_gbs": hbm_peak, "frac": ks_bytes * value / world / 1e9 / hbm_peak},
+            "roofline": {"kernel": top, "bound": "hbm", "achieved": achieved_top, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": None,
+                         "peak_source": peak_src},
+            "stages": stage_info,
+            "gpu_launches": 5 * args.steps,
+            "e2e": {"value": e2e_value, "unit": "ops/s",
+                    "h2d_bytes_per_step": Bsz * l1 * N * 4, "d2h_bytes_per_step": Bsz * 2 * l1 * N * 4,
+                    "api": "paper_2512_11269_b200.keyswitch per ciphertext"},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--level", type=int, default=35)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -102,6 +102,14 @@ int lf_keyswitch(const lf_ctx* ctx, int level, const uint32_t* x, size_t x_bstri
                  const uint32_t* evk, size_t evk_bstride, uint32_t* out, size_t out_bstride,
                  int batch, void* workspace, void* stream);
 
+/* Measurement helper: lf_keyswitch with CUDA events recorded on `stream` around each of the
+ * five fused kernels; synchronises on the last event and writes their durations (ms) to
+ * stage_ms[0..4] = {modup_in, modup_bconv, ks_inner, moddown_bconv, moddown_out}. */
+int lf_keyswitch_profiled(const lf_ctx* ctx, int level, const uint32_t* x, size_t x_bstride,
+                          const uint32_t* evk, size_t evk_bstride, uint32_t* out,
+                          size_t out_bstride, int batch, void* workspace, void* stream,
+                          float* stage_ms);
+
 /* hom_mul (ckks.py:182-194): tensor product + relinearisation, no rescale. */
 int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t* ct2,
                size_t ct_bstride, const uint32_t* rlk, uint32_t* out, size_t out_bstride,

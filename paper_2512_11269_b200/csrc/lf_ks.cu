@@ -80,63 +80,159 @@ LF_DEV u32 bconv_u_smem(const u32* Yp, int ystride, const BconvDev& B) {
   return bconv_u_exact(y, B, (u32)r);
 }
 
-template <int L1, int L2, int CW>
-__global__ void __launch_bounds__(CW * LineCfg<L1>::T)
-k_bconv_colpass(BcArgs A, LfDev dv, int kmax) {
-  using C = LineCfg<L1>;
-  constexpr int M1 = C::M;
-  extern __shared__ u32 sm[];
-  u32* Y = sm;                                   // [kmax][M1][CW]
-  u32* X = sm + (size_t)kmax * M1 * CW;          // exchange
-  const BcGroupDev& G = A.g[blockIdx.y / A.tsplit];
-  const int ts = blockIdx.y % A.tsplit;
-  const BconvDev& B = G.B;
-  const int c = threadIdx.x % CW, tl = threadIdx.x / CW;
-  const int col = blockIdx.x * CW + c;
-  const u32* src = A.src + (size_t)blockIdx.z * A.src_bs;
-  u32* dst = A.dst + (size_t)blockIdx.z * A.dst_bs;
-  const AddrC<L1, CW> addr{c};
-  const int logN = L1 + L2;
+// Shared-memory tile of the converted sources: Y[i][tl][c][YP] with YP = E + 4 words, so a
+// thread's E values are contiguous (LDS.128/STS.128) and the 8 threads of a quarter-warp
+// (consecutive c) hit disjoint bank quads.
+template <int L1>
+struct YTile {
+  static constexpr int E = LineCfg<L1>::E;
+  static constexpr int T = LineCfg<L1>::T;
+  static constexpr int YP = (E % 4 == 0) ? E + 4 : E;
+};
 
-  // phase 1: INTT column pass of every source row, y_i = r_i * c_i mod s_i into shared memory
-  for (int i = 0; i < B.k; ++i) {
+// Barrier over one thread group (named barrier when the group is whole warps; otherwise the
+// CTA has a single group and __syncthreads is used).
+template <bool NAMED>
+struct SyncGroup {
+  int id, n;
+  LF_DEV void operator()() const {
+    if (NAMED) asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    else __syncthreads();
+  }
+};
+
+template <int E>
+LF_DEV void lds_vec(u32* v, const u32* p) {
+  if constexpr (E % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q) {
+      const uint4 t = *reinterpret_cast<const uint4*>(p + 4 * q);
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < E; ++q) v[q] = p[q];
+  }
+}
+template <int E>
+LF_DEV void sts_vec(u32* p, const u32* v) {
+  if constexpr (E % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q)
+      *reinterpret_cast<uint4*>(p + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < E; ++q) p[q] = v[q];
+  }
+}
+
+// grid.x = batch (fastest) x column tiles x (groups * tsplit); TG thread groups share the tile.
+template <int L1, int L2, int CW, int KMAX, int TG>
+__global__ void __launch_bounds__(TG * CW * LineCfg<L1>::T)
+k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
+  using C = LineCfg<L1>;
+  using Y_ = YTile<L1>;
+  constexpr int E = C::E, T = C::T, YP = Y_::YP;
+  constexpr int GT = CW * T;
+  constexpr int NCT = (1 << L2) / CW;
+  constexpr int logN = L1 + L2;
+  extern __shared__ __align__(16) u32 sm[];
+  const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
+  const int c = lt % CW, tl = lt / CW;
+  int bid = blockIdx.x;
+  const int b = bid % nbatch;
+  bid /= nbatch;
+  const int ct = bid % NCT;
+  const int gy = bid / NCT;
+  const BcGroupDev& G = A.g[gy / A.tsplit];
+  const int ts = gy % A.tsplit;
+  const BconvDev& B = G.B;
+  const int k = B.k;
+  const int col = ct * CW + c;
+  u32* Ybase = sm + (size_t)(tl * CW + c) * YP;                 // + i * T*CW*YP
+  constexpr int YI = T * CW * YP;                              // words per source
+  u32* X = sm + (size_t)kmax * YI + grp * smemC_words<L1, CW>();
+  const u32* src = A.src + (size_t)b * A.src_bs;
+  u32* dst = A.dst + (size_t)b * A.dst_bs;
+  const AddrC<L1, CW> addr{c};
+  static_assert(TG == 1 || GT % 32 == 0, "thread groups must be whole warps");
+  const SyncGroup<GT % 32 == 0> gsync{1 + grp, GT};
+
+  // phase 1: INTT column pass of each source row (sources split over the groups)
+  for (int i = grp; i < k; i += TG) {
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
-    const u32* s = src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col;
-    u32 x[C::E];
-    load_col_step2<L1, L2>(x, s, tl);
-    inv_line<L1>(x, 1u, dv.twi + ((size_t)pi << logN), pk.q, X, tl, addr, SyncBlock{});
+    u32 x[E];
+    load_col_step2<L1, L2>(x, src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col, tl);
+    inv_line<L1>(x, 1u, dv.twi + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
-    for (int j = 0; j < C::E; ++j)
-      Y[((size_t)i * M1 + tl + C::T * j) * CW + c] = mul_shoup(x[j], ci, cpi, pk.q);
-    __syncthreads();
+    for (int j = 0; j < E; ++j) x[j] = mul_shoup(x[j], ci, cpi, pk.q);
+    sts_vec<E>(Ybase + (size_t)i * YI, x);
+    gsync();
   }
-  // phase 2: exact overflow counts for this thread's positions
-  u32 u[C::E];
-#pragma unroll
-  for (int j = 0; j < C::E; ++j)
-    u[j] = bconv_u_smem(Y + (size_t)(tl + C::T * j) * CW + c, M1 * CW, B);
+  __syncthreads();
 
-  // phase 3: per target: BConv -> NTT column pass -> T1
+  // phase 2: exact overflow counts u for this thread's E positions (float64 fast path)
+  u32 u[E];
+  {
+    double v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      if (i < k) {
+        u32 y[E];
+        lds_vec<E>(y, Ybase + (size_t)i * YI);
+        const double is = B.inv_s[i];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = fma((double)y[j], is, v[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const double r = rint(v[j]);
+      if (fabs(v[j] - r) >= 0x1p-40) {
+        u[j] = (u32)floor(v[j]);
+      } else {
+        u32 yy[64];
+        bool z = true;
+        for (int i = 0; i < k; ++i) {
+          yy[i] = Ybase[(size_t)i * YI + j];
+          z &= yy[i] == 0;
+        }
+        u[j] = z ? 0u : bconv_u_exact(yy, B, (u32)r);
+      }
+    }
+  }
+
+  // phase 3: targets of this split, round-robin over the groups: BConv -> NTT column pass
   const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
-  for (int t = t0; t < t1; ++t) {
+  for (int t = t0 + grp; t < t1; t += TG) {
     const int pi = B.tgt_pi[t];
     const PrimeK pk = dv.pk[pi];
-    const u32* wt = B.w + (size_t)t * B.k;
+    const u32* wt = B.w + (size_t)t * k;
     const u32 ns = B.negS[t];
-    u32 x[C::E];
+    u64 acc[E];
 #pragma unroll
-    for (int j = 0; j < C::E; ++j) {
-      const u32* yp = Y + (size_t)(tl + C::T * j) * CW + c;
-      u64 acc = (u64)u[j] * ns;
-      for (int i = 0; i < B.k; ++i) acc += (u64)yp[(size_t)i * M1 * CW] * __ldg(&wt[i]);
-      x[j] = reduce64(acc, pk);
+    for (int j = 0; j < E; ++j) acc[j] = (u64)u[j] * ns;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      if (i < k) {
+        const u32 wv = __ldg(&wt[i]);
+        u32 y[E];
+        lds_vec<E>(y, Ybase + (size_t)i * YI);
+#pragma unroll
+        for (int j = 0; j < E; ++j) acc[j] += (u64)y[j] * wv;
+      }
     }
-    fwd_line<L1, 1>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, SyncBlock{});
+    u32 x[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) x[j] = reduce64(acc[j], pk);
+    fwd_line<L1, 1>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
     store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
-    __syncthreads();
+    gsync();
   }
 }
 
@@ -153,6 +249,7 @@ struct KsInnerArgs {
   const u32* rowk;     // plan: per main row {s, s', pinv, pinv'}
   int level, d, beta, L, alpha, R;
   u32 g;               // galois element (GALOIS mode)
+  int nbatch;          // grid.x = batch (fastest, so a key line is reused from L2) x lines
 };
 
 template <int L1, int L2, bool GALOIS, int XMODE>
@@ -166,8 +263,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   extern __shared__ u32 sm[];
   const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
   const int groups = (1 << L1) / S::LPCR;
-  const int t = blockIdx.x / groups;                         // ext position
-  const int hi = (blockIdx.x % groups) * S::LPCR + ln;
+  const size_t b = blockIdx.x % A.nbatch;
+  const int bl = blockIdx.x / A.nbatch;
+  const int t = bl / groups;                                 // ext position
+  const int hi = (bl % groups) * S::LPCR + ln;
   const int l = A.level;
   const bool is_main = t <= l;
   const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index == key row
@@ -176,7 +275,6 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   u32* xs = sm + ln * (pitchR<L2>() + M2);
   u32* perm_buf = xs + pitchR<L2>();
   const AddrR<L2> addr{0};
-  const size_t b = blockIdx.z;
 
   int hs = hi;
   if (GALOIS) hs = (int)(auto_src_index((u32)hi << L2, A.g, logN) >> L2);
@@ -391,27 +489,29 @@ static KsWs carve(const LfCtx* ctx, int level, void* ws) {
   return w;
 }
 
-template <int L1, int L2, int CW>
+template <int L1, int L2, int CW, int KMAX, int TG>
 static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
-  const size_t sm = ((size_t)kmax * LineCfg<L1>::M * CW + smemC_words<L1, CW>()) * 4;
+  using Y_ = YTile<L1>;
+  const size_t sm = ((size_t)kmax * Y_::T * CW * Y_::YP + (size_t)TG * smemC_words<L1, CW>()) * 4;
   if (sm > 227 * 1024) { lf_set_error("bconv: shared memory %zu too large", sm); return 2; }
-  auto kern = k_bconv_colpass<L1, L2, CW>;
+  auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((1 << L2) / CW, A.ngroups * A.tsplit, batch);
-  kern<<<grid, CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax);
+  const long nblocks = (long)batch * ((1 << L2) / CW) * A.ngroups * A.tsplit;
+  kern<<<(unsigned)nblocks, TG * CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax, batch);
   LF_CHECK_LAUNCH();
   return 0;
 }
 
+// Column tile width and group count: CW = 8 columns (32-byte row segments) and two thread
+// groups sharing the source tile for the production sizes; narrower tiles for large digit
+// counts (d = 1 style parameter sets) or tiny rings.
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   constexpr int NCOL = 1 << L2;
-  // columns per CTA: 8 when the source tile fits, fewer for large digit sizes
-  const size_t per_col = (size_t)kmax * LineCfg<L1>::M * 4;
-  if (NCOL >= 8 && per_col * 8 <= 160 * 1024) return launch_bc<L1, L2, (NCOL >= 8 ? 8 : 1)>(ctx, A, batch, kmax, s);
-  if (NCOL >= 4 && per_col * 4 <= 200 * 1024) return launch_bc<L1, L2, (NCOL >= 4 ? 4 : 1)>(ctx, A, batch, kmax, s);
-  if (NCOL >= 2 && per_col * 2 <= 210 * 1024) return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1)>(ctx, A, batch, kmax, s);
-  return launch_bc<L1, L2, 1>(ctx, A, batch, kmax, s);
+  constexpr int CW8 = NCOL >= 8 ? 8 : NCOL;
+  constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 2 : 1;
+  if (kmax <= 16) return launch_bc<L1, L2, CW8, 16, TG>(ctx, A, batch, kmax, s);
+  return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1), 64, 1>(ctx, A, batch, kmax, s);
 }
 
 static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax) {
@@ -437,7 +537,8 @@ struct KsCall {
 };
 
 template <int L1, int L2>
-static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t s) {
+static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t s,
+                       cudaEvent_t* ev = nullptr) {
   using S = NttShape<L1, L2>;
   const LfKsPlan* P = ctx->ks;
   const KsLevelPlan& K = P->lv[c.level];
@@ -448,6 +549,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
   const int groups = (1 << L1) / S::LPCR;
 
+#define LF_MARK(i) do { if (ev) cudaEventRecord(ev[i], s); } while (0)
+  LF_MARK(0);
   // K_A
   {
     const int nlines = l1 << L1;
@@ -458,6 +561,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
       k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1);
     LF_CHECK_LAUNCH();
   }
+  LF_MARK(1);
   // K_BC (ModUp)
   {
     BcArgs A{};
@@ -472,20 +576,22 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.tsplit = bc_tsplit(K.beta, c.batch, (1 << L2) / 8, mmax);
     if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, kmax, s)) return e;
   }
+  LF_MARK(2);
   // K_C
   {
     KsInnerArgs A{};
     A.T1 = w.T1; A.x = c.x; A.x2 = c.x2; A.key = c.key; A.acc = w.acc; A.T2 = w.T2;
     A.t1_bs = w.per; A.x_bs = c.x_bs; A.key_bs = c.key_bs; A.acc_bs = w.per; A.t2_bs = w.per;
     A.rowk = P->rowk; A.level = c.level; A.d = P->d; A.beta = K.beta; A.L = P->L; A.alpha = alpha;
-    A.R = P->L + 1 + alpha; A.g = c.g;
+    A.R = P->L + 1 + alpha; A.g = c.g; A.nbatch = c.batch;
     const size_t smC = (size_t)S::LPCR * (pitchR<L2>() + LineCfg<L2>::M) * 4;
-    dim3 grid(K.ext * groups, 1, c.batch);
+    dim3 grid(K.ext * groups * c.batch);
     if (c.op == OP_ROT) k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv);
     else if (c.op == OP_MUL) k_ks_inner<L1, L2, false, 1><<<grid, S::TRR, smC, s>>>(A, dv);
     else k_ks_inner<L1, L2, false, 0><<<grid, S::TRR, smC, s>>>(A, dv);
     LF_CHECK_LAUNCH();
   }
+  LF_MARK(3);
   // K_BC (ModDown)
   {
     BcArgs A{};
@@ -502,6 +608,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, l1);
     if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, alpha, s)) return e;
   }
+  LF_MARK(4);
   // K_E
   {
     ModDownArgs A{};
@@ -514,6 +621,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     else k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv);
     LF_CHECK_LAUNCH();
   }
+  LF_MARK(5);
+#undef LF_MARK
   (void)N;
   return 0;
 }
@@ -607,8 +716,9 @@ static int ks_check(const lf_ctx* ctx, int level) {
   return 0;
 }
 
-static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s) {
-#define LF_KS(A, B) { if (int e = ks_pipeline<A, B>(ctx, c, ws, s)) return e; }
+static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
+                  cudaEvent_t* ev = nullptr) {
+#define LF_KS(A, B) { if (int e = ks_pipeline<A, B>(ctx, c, ws, s, ev)) return e; }
   LF_DISPATCH_LOGN(ctx->logN, LF_KS)
 #undef LF_KS
   return 0;
@@ -664,6 +774,27 @@ int lf_rotate(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstrid
   c.out = out; c.out_bs = out_bstride; c.e0 = ct; c.e1 = nullptr; c.e_bs = ct_bstride;
   c.g = g & ((2u << ctx->logN) - 1);
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_keyswitch_profiled(const lf_ctx* ctx, int level, const uint32_t* x, size_t x_bstride,
+                          const uint32_t* evk, size_t evk_bstride, uint32_t* out,
+                          size_t out_bstride, int batch, void* workspace, void* stream,
+                          float* stage_ms) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!x || !evk || !out || !workspace || !stage_ms) { lf_set_error("lf_keyswitch_profiled: null argument"); return 1; }
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_KS;
+  c.x = x; c.x2 = x; c.x_bs = x_bstride; c.key = evk; c.key_bs = evk_bstride;
+  c.out = out; c.out_bs = out_bstride;
+  cudaEvent_t ev[6];
+  for (auto& e : ev) cudaEventCreate(&e);
+  int rc = run_ks(ctx, c, workspace, (cudaStream_t)stream, ev);
+  if (!rc) {
+    cudaEventSynchronize(ev[5]);
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&stage_ms[i], ev[i], ev[i + 1]);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
 }
 
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch) {

@@ -99,3 +99,16 @@ def keyswitch_batch(params, level: int, xs: torch.Tensor, evk, out: torch.Tensor
                                              dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
                   "lf_keyswitch")
     return out
+
+
+def keyswitch_batch_profiled(params, level: int, xs: torch.Tensor, evk, out: torch.Tensor,
+                             ws: torch.Tensor):
+    """As keyswitch_batch, returning the CUDA-event duration (ms) of each fused kernel:
+    [modup_in, modup_bconv, ks_inner, moddown_bconv, moddown_out]."""
+    import ctypes
+    ctx = get_context(params)
+    ms = (ctypes.c_float * 5)()
+    _native.check(_native.lib().lf_keyswitch_profiled(
+        ctx.handle, level, dptr(xs), xs[0].numel(), dptr(evk.data), 0, dptr(out), out[0].numel(),
+        xs.shape[0], dptr(ws), stream_handle(), ms), "lf_keyswitch_profiled")
+    return list(ms)
