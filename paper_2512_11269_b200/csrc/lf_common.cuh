@@ -51,5 +51,12 @@ inline void lf_split(int logN, int& L1, int& L2) {
   L2 = logN - L1;
 }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory.
+template <class K>
+inline void lf_smem_optin(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 // host launchers (lf_ntt.cu)
 int lf_launch_ntt(const LfCtx* ctx, u32* rows, const RowMap& rm, bool inverse, cudaStream_t s);

@@ -23,6 +23,12 @@
 
 #define LF_BC_MAXG 16
 
+// Bulk L2 prefetch (TMA engine, sm_90+): warms the next stage's contiguous row segment so the
+// per-thread loads that follow hit L2 instead of HBM.  bytes must be a multiple of 16.
+LF_DEV void prefetch_l2(const void* p, u32 bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 struct BcArgs {
   const u32* src;
   u32* dst;
@@ -34,21 +40,20 @@ struct BcArgs {
 // ---------------------------------------------------------------------------------------
 // K_A: row pass of the inverse NTT.  MODE 0: rows of x; MODE 1: rows of a1*a2 (tensor d2).
 template <int L1, int L2, int MODE>
-__global__ void __launch_bounds__(NttShape<L1, L2>::TR)
+__global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
            size_t x_bs, size_t t_bs, int nrows, LfDev dv, int src_rs, int src_r0, int pfix) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
-  extern __shared__ u32 sm[];
+  constexpr int GROUPS = (1 << L1) / S::LPCR;
+  extern __shared__ __align__(16) u32 sm[];
   const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
-  const int nlines = nrows << L1;
-  int line = blockIdx.x * S::LPC + ln;
-  const bool valid = line < nlines;
-  if (!valid) line = nlines - 1;
-  const int row = line >> L1, hi = line & ((1 << L1) - 1);
+  const int row = blockIdx.x / GROUPS, hi0 = (blockIdx.x % GROUPS) * S::LPCR, hi = hi0 + ln;
   const int pi = pfix >= 0 ? pfix : row;
   const PrimeK pk = dv.pk[pi];
-  const uint2* tw = dv.twi + ((size_t)pi << (L1 + L2));
+  uint2* tws = reinterpret_cast<uint2*>(sm);
+  stage_tree_async<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR,
+                       threadIdx.x, blockDim.x);
   const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)(row * src_rs + src_r0) << (L1 + L2)) +
                      ((size_t)hi << L2);
   u32 v[C::E];
@@ -59,8 +64,12 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
 #pragma unroll
     for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
   }
-  inv_line<L2>(v, (1u << L1) + hi, tw, pk.q, sm, tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
-  if (valid) store_row_step1<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)line << L2), tl);
+  cp_async_wait_all();
+  __syncthreads();
+  inv_line<L2>(v, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
+               rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
+  store_row_step1<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)row << (L1 + L2)) +
+                             ((size_t)hi << L2), tl);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -80,14 +89,13 @@ LF_DEV u32 bconv_u_smem(const u32* Yp, int ystride, const BconvDev& B) {
   return bconv_u_exact(y, B, (u32)r);
 }
 
-// Shared-memory tile of the converted sources: Y[i][tl][c][YP] with YP = E + 4 words, so a
-// thread's E values are contiguous (LDS.128/STS.128) and the 8 threads of a quarter-warp
-// (consecutive c) hit disjoint bank quads.
+// Shared-memory tile of the converted sources: Y[i][tl][c][E].  A thread's E values are
+// contiguous (LDS.128/STS.128); the four 16-byte chunks of each 16-word block are rotated by
+// (c >> 1) so the 8 threads of a quarter-warp (consecutive c) hit 8 disjoint bank quads.
 template <int L1>
 struct YTile {
   static constexpr int E = LineCfg<L1>::E;
   static constexpr int T = LineCfg<L1>::T;
-  static constexpr int YP = (E % 4 == 0) ? E + 4 : E;
 };
 
 // Barrier over one thread group (named barrier when the group is whole warps; otherwise the
@@ -101,44 +109,56 @@ struct SyncGroup {
   }
 };
 
+// physical word offset of logical 4-word chunk lq of a thread slot
+LF_DEV int ychunk(int lq, int rot) { return 4 * ((lq + rot) & 3) + 16 * (lq >> 2); }
+
 template <int E>
-LF_DEV void lds_vec(u32* v, const u32* p) {
-  if constexpr (E % 4 == 0) {
+LF_DEV void y_load(u32* v, const u32* slot, int rot) {
+  if constexpr (E % 16 == 0) {
 #pragma unroll
     for (int q = 0; q < E / 4; ++q) {
-      const uint4 t = *reinterpret_cast<const uint4*>(p + 4 * q);
+      const uint4 t = *reinterpret_cast<const uint4*>(slot + ychunk(q, rot));
       v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < E; ++q) v[q] = p[q];
+    for (int q = 0; q < E; ++q) v[q] = slot[q];
   }
 }
 template <int E>
-LF_DEV void sts_vec(u32* p, const u32* v) {
-  if constexpr (E % 4 == 0) {
+LF_DEV void y_store(u32* slot, const u32* v, int rot) {
+  if constexpr (E % 16 == 0) {
 #pragma unroll
     for (int q = 0; q < E / 4; ++q)
-      *reinterpret_cast<uint4*>(p + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      *reinterpret_cast<uint4*>(slot + ychunk(q, rot)) =
+          make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   } else {
 #pragma unroll
-    for (int q = 0; q < E; ++q) p[q] = v[q];
+    for (int q = 0; q < E; ++q) slot[q] = v[q];
   }
+}
+
+// x < 2^64 -> [0, 4q) (lazy; the forward NTT accepts it with input bound 4)
+LF_DEV u32 reduce64_lazy4(u64 x, const PrimeK& k) {
+  const u32 hi = (u32)(x >> 32), lo = (u32)x;
+  return mul_shoup_lazy(hi, k.r32, k.r32p, k.q) + reduce32_lazy(lo, k);
 }
 
 // grid.x = batch (fastest) x column tiles x (groups * tsplit); TG thread groups share the tile.
 template <int L1, int L2, int CW, int KMAX, int TG>
-__global__ void __launch_bounds__(TG * CW * LineCfg<L1>::T)
+__global__ void __launch_bounds__(TG * CW * LineCfg<L1>::T, (TG * CW * LineCfg<L1>::T) >= 512 ? 2 : 1)
 k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   using C = LineCfg<L1>;
-  using Y_ = YTile<L1>;
-  constexpr int E = C::E, T = C::T, YP = Y_::YP;
+  constexpr int E = C::E, T = C::T;
   constexpr int GT = CW * T;
   constexpr int NCT = (1 << L2) / CW;
   constexpr int logN = L1 + L2;
+  constexpr int YI = T * CW * E;                               // words per source
+  constexpr int EH = E >= 16 ? E / 2 : E;                      // MAC in halves (registers)
   extern __shared__ __align__(16) u32 sm[];
   const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
   const int c = lt % CW, tl = lt / CW;
+  const int rot = c >> 1;
   int bid = blockIdx.x;
   const int b = bid % nbatch;
   bid /= nbatch;
@@ -149,8 +169,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const BconvDev& B = G.B;
   const int k = B.k;
   const int col = ct * CW + c;
-  u32* Ybase = sm + (size_t)(tl * CW + c) * YP;                 // + i * T*CW*YP
-  constexpr int YI = T * CW * YP;                              // words per source
+  u32* Ybase = sm + (size_t)(tl * CW + c) * E;
   u32* X = sm + (size_t)kmax * YI + grp * smemC_words<L1, CW>();
   const u32* src = A.src + (size_t)b * A.src_bs;
   u32* dst = A.dst + (size_t)b * A.dst_bs;
@@ -168,13 +187,13 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
     for (int j = 0; j < E; ++j) x[j] = mul_shoup(x[j], ci, cpi, pk.q);
-    sts_vec<E>(Ybase + (size_t)i * YI, x);
+    y_store<E>(Ybase + (size_t)i * YI, x, rot);
     gsync();
   }
   __syncthreads();
 
-  // phase 2: exact overflow counts u for this thread's E positions (float64 fast path)
-  u32 u[E];
+  // phase 2: exact overflow counts u (< 64) for this thread's E positions, packed 4 per word
+  u32 up[(E + 3) / 4];
   {
     double v[E];
 #pragma unroll
@@ -183,30 +202,38 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     for (int i = 0; i < KMAX; ++i) {
       if (i < k) {
         u32 y[E];
-        lds_vec<E>(y, Ybase + (size_t)i * YI);
+        y_load<E>(y, Ybase + (size_t)i * YI, rot);
         const double is = B.inv_s[i];
 #pragma unroll
         for (int j = 0; j < E; ++j) v[j] = fma((double)y[j], is, v[j]);
       }
     }
 #pragma unroll
+    for (int w = 0; w < (E + 3) / 4; ++w) up[w] = 0;
+#pragma unroll
     for (int j = 0; j < E; ++j) {
       const double r = rint(v[j]);
+      u32 uj;
       if (fabs(v[j] - r) >= 0x1p-40) {
-        u[j] = (u32)floor(v[j]);
+        uj = (u32)floor(v[j]);
       } else {
         u32 yy[64];
         bool z = true;
         for (int i = 0; i < k; ++i) {
-          yy[i] = Ybase[(size_t)i * YI + j];
+          const u32* slot = Ybase + (size_t)i * YI;
+          yy[i] = (E % 16 == 0) ? slot[ychunk(j / 4, rot) + (j % 4)] : slot[j];
           z &= yy[i] == 0;
         }
-        u[j] = z ? 0u : bconv_u_exact(yy, B, (u32)r);
+        uj = z ? 0u : bconv_u_exact(yy, B, (u32)r);
       }
+      up[j / 4] |= uj << (8 * (j % 4));
     }
   }
 
   // phase 3: targets of this split, round-robin over the groups: BConv -> NTT column pass
+  const u32* yq[4];                                    // rotated chunk bases (no per-load math)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) yq[q] = Ybase + 4 * ((q + rot) & 3);
   const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
   for (int t = t0 + grp; t < t1; t += TG) {
@@ -214,23 +241,38 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     const PrimeK pk = dv.pk[pi];
     const u32* wt = B.w + (size_t)t * k;
     const u32 ns = B.negS[t];
-    u64 acc[E];
-#pragma unroll
-    for (int j = 0; j < E; ++j) acc[j] = (u64)u[j] * ns;
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i) {
-      if (i < k) {
-        const u32 wv = __ldg(&wt[i]);
-        u32 y[E];
-        lds_vec<E>(y, Ybase + (size_t)i * YI);
-#pragma unroll
-        for (int j = 0; j < E; ++j) acc[j] += (u64)y[j] * wv;
-      }
-    }
     u32 x[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) x[j] = reduce64(acc[j], pk);
-    fwd_line<L1, 1>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
+    for (int h = 0; h < E / EH; ++h) {
+      u64 acc[EH];
+#pragma unroll
+      for (int j = 0; j < EH; ++j)
+        acc[j] = (u64)((up[(h * EH + j) / 4] >> (8 * ((h * EH + j) % 4))) & 0xFFu) * ns;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        if (i < k) {
+          const u32 wv = __ldg(&wt[i]);
+          const u32* slot = Ybase + (size_t)i * YI;
+          u32 y[EH];
+          if constexpr (E % 16 == 0) {
+#pragma unroll
+            for (int q = 0; q < EH / 4; ++q) {
+              const int lq = h * (EH / 4) + q;
+              const uint4 tv = *reinterpret_cast<const uint4*>(yq[lq & 3] + (size_t)i * YI + 16 * (lq >> 2));
+              y[4 * q] = tv.x; y[4 * q + 1] = tv.y; y[4 * q + 2] = tv.z; y[4 * q + 3] = tv.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < EH; ++j) y[j] = slot[h * EH + j];
+          }
+#pragma unroll
+          for (int j = 0; j < EH; ++j) acc[j] += (u64)y[j] * wv;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < EH; ++j) x[h * EH + j] = reduce64_lazy4(acc[j], pk);
+    }
+    fwd_line<L1, 4>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
     store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
     gsync();
   }
@@ -253,7 +295,7 @@ struct KsInnerArgs {
 };
 
 template <int L1, int L2, bool GALOIS, int XMODE>
-__global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
+__global__ void __launch_bounds__(NttShape<L1, L2>::TRR, 2)
 k_ks_inner(KsInnerArgs A, LfDev dv) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
@@ -272,18 +314,45 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index == key row
   const PrimeK pk = dv.pk[pi];
   const int ext = l + 1 + A.alpha;
-  u32* xs = sm + ln * (pitchR<L2>() + M2);
+  u32* xs = rowpass_xs<L1, L2>(sm) + ln * (pitchR<L2>() + M2);
   u32* perm_buf = xs + pitchR<L2>();
   const AddrR<L2> addr{0};
 
   int hs = hi;
   if (GALOIS) hs = (int)(auto_src_index((u32)hi << L2, A.g, logN) >> L2);
+  // twiddle subtrees of this CTA's source lines.  The automorphism maps an aligned block of
+  // LPCR lines onto an aligned block of LPCR lines, so one staged block serves all of them.
+  uint2* tws = reinterpret_cast<uint2*>(sm);
+  int hi0s = (bl % groups) * S::LPCR;
+  if (GALOIS)
+    hi0s = (int)((auto_src_index((u32)hi0s << L2, A.g, logN) >> L2) / S::LPCR) * S::LPCR;
+  stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
+                       threadIdx.x, blockDim.x);
+  cp_async_wait_all();
+  __syncthreads();
 
   u64 accb[C::E], acca[C::E];
 #pragma unroll
   for (int e = 0; e < C::E; ++e) { accb[e] = 0; acca[e] = 0; }
 
+  const int hi0 = (bl % groups) * S::LPCR;
+  constexpr u32 SEG = (u32)S::LPCR << L2;                     // words of this CTA's lines
+  auto prefetch_digit = [&](int j) {
+    if (threadIdx.x == 0 && j < A.beta) {
+      const size_t lo0 = (size_t)hi0 << L2;
+      if (!(is_main && (t % A.d) == j))
+        prefetch_l2(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + lo0, SEG * 4);
+      prefetch_l2(A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo0, SEG * 4);
+      prefetch_l2(A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo0, SEG * 4);
+    }
+  };
+  (void)prefetch_digit;
   for (int j = 0; j < A.beta; ++j) {
+    u32 kvb[C::E], kva[C::E];
+    load_row_step2<L2>(kvb, A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) +
+                                ((size_t)hi << L2), tl);
+    load_row_step2<L2>(kva, A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) +
+                                ((size_t)hi << L2), tl);
     u32 pc[C::E];
     if (is_main && (t % A.d) == j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
@@ -301,8 +370,8 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     } else {
       const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
       load_row_step1<L2>(pc, tr, tl);
-      fwd_line<L2, BIN>(pc, (1u << L1) + hs, dv.twf + ((size_t)pi << logN), pk.q, xs, tl, addr,
-                        SyncWarp{});
+      fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
+                        tl, addr, SyncWarp{});
       if (GALOIS) {
 #pragma unroll
         for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
@@ -318,15 +387,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e) pc[e] = reduce32_lazy(pc[e], pk);
     }
-    const u32* kb = A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2);
-    const u32* ka = A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2);
-    u32 kv[C::E];
-    load_row_step2<L2>(kv, kb, tl);
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kv[e];
-    load_row_step2<L2>(kv, ka, tl);
+    for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kvb[e];
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kv[e];
+    for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kva[e];
   }
   u32 rb[C::E], ra[C::E];
 #pragma unroll
@@ -376,7 +440,11 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   const int hi = (blockIdx.x % groups) * S::LPCR + ln;
   const PrimeK pk = dv.pk[t];
   const u32 sc = A.scal[t * A.sstride], scp = A.scal[t * A.sstride + 1];
-  const uint2* tw = dv.twf + ((size_t)t << logN);
+  uint2* tws = reinterpret_cast<uint2*>(sm);
+  const u32 R0 = (1u << L1) + (blockIdx.x % groups) * S::LPCR;
+  stage_tree_async<L2>(tws, dv.twf + ((size_t)t << logN), R0, S::LPCR, threadIdx.x, blockDim.x);
+  const TwTree tw{tws, R0, S::LPCR};
+  u32* xs = rowpass_xs<L1, L2>(sm);
   const AddrR<L2> addr{ln * pitchR<L2>()};
   const size_t b = blockIdx.z;
   const size_t lo0 = ((size_t)hi << L2);
@@ -384,8 +452,13 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   for (int p = 0; p < 2; ++p) {
     u32 cv[C::E], av[C::E];
     load_row_step1<L2>(cv, A.T3 + b * A.t3_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
-    if (p) __syncwarp();
-    fwd_line<L2, BIN>(cv, (1u << L1) + hi, tw, pk.q, sm, tl, addr, SyncWarp{});
+    if (p) {
+      __syncwarp();
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    fwd_line<L2, BIN>(cv, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
     load_row_step2<L2>(av, A.acc + b * A.acc_bs + ((size_t)(p * A.nacc + t) << logN) + lo0, tl);
 #pragma unroll
     for (int e = 0; e < C::E; ++e) {
@@ -452,8 +525,8 @@ k_pieces(const u32* __restrict__ T1, const u32* __restrict__ x, u32* __restrict_
     for (int e = 0; e < C::E; ++e) v[e] = mul_shoup(v[e], rowk[4 * t], rowk[4 * t + 1], pk.q);
   } else {
     load_row_step1<L2>(v, T1 + ((size_t)r << logN) + lo0, tl);
-    fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi, dv.twf + ((size_t)pi << logN), pk.q, sm, tl,
-                               AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
+    fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi, dv.twf + ((size_t)pi << logN), pk.q,
+                               rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
 #pragma unroll
     for (int e = 0; e < C::E; ++e) v[e] = reduce32(v[e], pk);
   }
@@ -492,7 +565,7 @@ static KsWs carve(const LfCtx* ctx, int level, void* ws) {
 template <int L1, int L2, int CW, int KMAX, int TG>
 static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   using Y_ = YTile<L1>;
-  const size_t sm = ((size_t)kmax * Y_::T * CW * Y_::YP + (size_t)TG * smemC_words<L1, CW>()) * 4;
+  const size_t sm = ((size_t)kmax * Y_::T * CW * Y_::E + (size_t)TG * smemC_words<L1, CW>()) * 4;
   if (sm > 227 * 1024) { lf_set_error("bconv: shared memory %zu too large", sm); return 2; }
   auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -509,7 +582,7 @@ template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   constexpr int NCOL = 1 << L2;
   constexpr int CW8 = NCOL >= 8 ? 8 : NCOL;
-  constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 2 : 1;
+  constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 4 : 1;
   if (kmax <= 16) return launch_bc<L1, L2, CW8, 16, TG>(ctx, A, batch, kmax, s);
   return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1), 64, 1>(ctx, A, batch, kmax, s);
 }
@@ -546,19 +619,18 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   const size_t N = ctx->N;
   const KsWs w = carve(ctx, c.level, ws);
   const LfDev dv = ctx->dev();
-  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
 
 #define LF_MARK(i) do { if (ev) cudaEventRecord(ev[i], s); } while (0)
   LF_MARK(0);
   // K_A
   {
-    const int nlines = l1 << L1;
-    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, c.batch);
+    dim3 grid(l1 * groups, 1, c.batch);
     if (c.op == OP_MUL)
-      k_modup_in<L1, L2, 1><<<grid, S::TR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1);
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1); }
     else
-      k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1);
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -584,11 +656,11 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.t1_bs = w.per; A.x_bs = c.x_bs; A.key_bs = c.key_bs; A.acc_bs = w.per; A.t2_bs = w.per;
     A.rowk = P->rowk; A.level = c.level; A.d = P->d; A.beta = K.beta; A.L = P->L; A.alpha = alpha;
     A.R = P->L + 1 + alpha; A.g = c.g; A.nbatch = c.batch;
-    const size_t smC = (size_t)S::LPCR * (pitchR<L2>() + LineCfg<L2>::M) * 4;
+    const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
     dim3 grid(K.ext * groups * c.batch);
-    if (c.op == OP_ROT) k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv);
-    else if (c.op == OP_MUL) k_ks_inner<L1, L2, false, 1><<<grid, S::TRR, smC, s>>>(A, dv);
-    else k_ks_inner<L1, L2, false, 0><<<grid, S::TRR, smC, s>>>(A, dv);
+    if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv); }
+    else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, false, 1>, smC); k_ks_inner<L1, L2, false, 1><<<grid, S::TRR, smC, s>>>(A, dv); }
+    else { lf_smem_optin(k_ks_inner<L1, L2, false, 0>, smC); k_ks_inner<L1, L2, false, 0><<<grid, S::TRR, smC, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(3);
@@ -616,9 +688,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1; A.g = c.g;
     dim3 grid(l1 * groups, 1, c.batch);
-    if (c.op == OP_MUL) k_moddown_out<L1, L2, EPI_MUL><<<grid, S::TRR, smR, s>>>(A, dv);
-    else if (c.op == OP_ROT) k_moddown_out<L1, L2, EPI_ROT><<<grid, S::TRR, smR, s>>>(A, dv);
-    else k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv);
+    if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); k_moddown_out<L1, L2, EPI_MUL><<<grid, S::TRR, smR, s>>>(A, dv); }
+    else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); k_moddown_out<L1, L2, EPI_ROT><<<grid, S::TRR, smR, s>>>(A, dv); }
+    else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(5);
@@ -636,15 +708,14 @@ static int rescale_pipeline(const LfCtx* ctx, int level, const u32* ct, size_t c
   const int l = level;
   const size_t N = ctx->N;
   const LfDev dv = ctx->dev();
-  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
   u32* T2 = (u32*)ws;                      // per instance: 2 rows, then T3: 2 l rows
   const size_t per = (2 + 2 * (size_t)l) * N;
   u32* T3 = T2 + 2 * N;
   {  // row pass of INTT(b_l), INTT(a_l)  (poly.py:284-287 -> mod_down of the top prime)
-    const int nlines = 2 << L1;
-    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, batch);
-    k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2, dv, l + 1, l, l);
+    dim3 grid(2 * groups, 1, batch);
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2, dv, l + 1, l, l); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -663,7 +734,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, const u32* ct, size_t c
     A.scal = P->qinv + (size_t)l * P->n_main * 2; A.sstride = 2;
     A.nt = l; A.nacc = l + 1; A.ne = 0; A.g = 0;
     dim3 grid(l * groups, 1, batch);
-    k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv);
+    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
   }
   return 0;
@@ -678,12 +749,11 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int l1 = level + 1;
   const KsWs w = carve(ctx, level, ws);
   const LfDev dv = ctx->dev();
-  const size_t smR = (size_t)S::LPC * pitchR<L2>() * 4;
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
   {
-    const int nlines = l1 << L1;
-    dim3 grid((nlines + S::LPC - 1) / S::LPC, 1, 1);
-    k_modup_in<L1, L2, 0><<<grid, S::TR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, 1, 0, -1);
+    dim3 grid(l1 * groups, 1, 1);
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, 1, 0, -1); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -700,6 +770,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   }
   {
     dim3 grid(K.beta * K.ext * groups);
+    lf_smem_optin(k_pieces<L1, L2>, smR);
     k_pieces<L1, L2><<<grid, S::TRR, smR, s>>>(w.T1, x, pieces, P->rowk, level, P->d, P->L,
                                               P->n_special, dv);
     LF_CHECK_LAUNCH();

@@ -42,18 +42,98 @@ __host__ __device__ constexpr int fwd_next_bound(int b) { return (fwd_needs_corr
 __host__ __device__ constexpr int fwd_bound_at(int b, int stages) {
   return stages == 0 ? b : fwd_bound_at(fwd_next_bound(b), stages - 1);
 }
+// bit k set <=> stage k (starting from bound b) must correct X first.  Used through a
+// constexpr variable so the per-stage decision folds away after unrolling.
+__host__ __device__ constexpr unsigned fwd_corr_mask(int b, int stages) {
+  unsigned m = 0;
+  for (int k = 0; k < stages; ++k) {
+    if (fwd_needs_corr(b)) m |= 1u << k;
+    b = fwd_next_bound(b);
+  }
+  return m;
+}
 
-// Forward CT sub-transform of 2^K registers.  Input bound BIN (units of q).
-template <int K, int BIN>
-LF_DEV void ct_sub(u32* x, u32 root, const uint2* __restrict__ tw, u32 q) {
+// ---- twiddle sources --------------------------------------------------------------------
+// get(depth, node): twiddle {w, w'} of heap node `node`, which sits `depth` levels below the
+// line root.  TwGlobal reads the per-prime table in HBM/L2; TwTree reads a CTA's staged copy of
+// the subtrees under roots R0 .. R0+span-1 (row passes); TwFlat reads a staged copy of the
+// first 2^L1 nodes (column passes, root 1).
+struct TwGlobal {
+  const uint2* p;
+  LF_DEV uint2 get(int, u32 n) const { return __ldg(&p[n]); }
+};
+struct TwTree {
+  const uint2* s;
+  u32 R0;
+  int span;
+  LF_DEV uint2 get(int d, u32 n) const { return s[span * ((1 << d) - 1) + (n - (R0 << d))]; }
+};
+struct TwFlat {
+  const uint2* s;
+  LF_DEV uint2 get(int, u32 n) const { return s[n]; }
+};
+
+// Stage the subtrees (LP levels) under roots R0..R0+span-1 of table `tab` into smem `dst`
+// (span * (2^LP - 1) entries), cooperatively and coalesced.  Caller syncs afterwards.
+template <int LP>
+LF_DEV void stage_tree(uint2* dst, const uint2* __restrict__ tab, u32 R0, int span, int tid,
+                       int nthr) {
+#pragma unroll
+  for (int d = 0; d < LP; ++d) {
+    const uint2* src = tab + ((size_t)R0 << d);
+    uint2* o = dst + span * ((1 << d) - 1);
+    const int n = span << d;
+    if ((n & 1) == 0 && (((size_t)R0 << d) & 1) == 0 && ((span * ((1 << d) - 1)) & 1) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* o4 = reinterpret_cast<uint4*>(o);
+      for (int i = tid; i < n / 2; i += nthr) o4[i] = __ldg(&s4[i]);
+    } else {
+      for (int i = tid; i < n; i += nthr) o[i] = __ldg(&src[i]);
+    }
+  }
+}
+// Asynchronous variant (cp.async, no register round trip): the copies land while the thread
+// goes on issuing its data loads; call cp_async_wait_all() + a barrier before reading.
+LF_DEV void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+LF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int LP>
+LF_DEV void stage_tree_async(uint2* dst, const uint2* __restrict__ tab, u32 R0, int span, int tid,
+                             int nthr) {
+#pragma unroll
+  for (int d = 0; d < LP; ++d) {
+    const uint2* src = tab + ((size_t)R0 << d);
+    uint2* o = dst + span * ((1 << d) - 1);
+    const int n = span << d;
+    if ((n & 1) == 0 && (((size_t)R0 << d) & 1) == 0 && ((span * ((1 << d) - 1)) & 1) == 0) {
+      for (int i = tid; i < n / 2; i += nthr) cp_async16(o + 2 * i, src + 2 * i);
+    } else {
+      for (int i = tid; i < n; i += nthr) o[i] = __ldg(&src[i]);
+    }
+  }
+}
+
+template <int M>
+LF_DEV void stage_flat(uint2* dst, const uint2* __restrict__ tab, int tid, int nthr) {
+  for (int i = tid; i < M; i += nthr) dst[i] = __ldg(&tab[i]);
+}
+
+// Forward CT sub-transform of 2^K registers.  Input bound BIN (units of q).  DOFF = depth of
+// `root` below the line root.
+template <int K, int BIN, int DOFF = 0, class TW>
+LF_DEV void ct_sub(u32* x, u32 root, const TW& tw, u32 q) {
   static_assert(BIN <= 16, "input bound too large");
+  constexpr unsigned CORR = fwd_corr_mask(BIN, K);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int h = 1 << (K - 1 - k);
-    const bool corr = fwd_needs_corr(fwd_bound_at(BIN, k));
+    const bool corr = (CORR >> k) & 1u;
 #pragma unroll
     for (int blk = 0; blk < (1 << k); ++blk) {
-      const uint2 w = __ldg(&tw[(root << k) + blk]);
+      const uint2 w = tw.get(DOFF + k, (root << k) + blk);
 #pragma unroll
       for (int j = 0; j < h; ++j) {
         u32 X = x[blk * 2 * h + j];
@@ -68,14 +148,14 @@ LF_DEV void ct_sub(u32* x, u32 root, const uint2* __restrict__ tw, u32 q) {
 }
 
 // Inverse GS sub-transform of 2^K registers, Harvey butterflies, [0,2q) in and out.
-template <int K>
-LF_DEV void gs_sub(u32* x, u32 root, const uint2* __restrict__ tw, u32 q) {
+template <int K, int DOFF = 0, class TW>
+LF_DEV void gs_sub(u32* x, u32 root, const TW& tw, u32 q) {
 #pragma unroll
   for (int k = K - 1; k >= 0; --k) {
     const int h = 1 << (K - 1 - k);
 #pragma unroll
     for (int blk = 0; blk < (1 << k); ++blk) {
-      const uint2 w = __ldg(&tw[(root << k) + blk]);
+      const uint2 w = tw.get(DOFF + k, (root << k) + blk);
 #pragma unroll
       for (int j = 0; j < h; ++j) {
         const u32 X = x[blk * 2 * h + j];
@@ -118,26 +198,36 @@ LF_DEV void xchg_21(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
 
 // Forward line: x in step-1 layout (bound BIN) -> step-2 layout (bound FwdLineBound).
 // The caller must make sure `sm` is free to overwrite (pre-sync) when needed.
-template <int LP, int BIN, class Addr, class Sync>
-LF_DEV void fwd_line(u32* x, u32 root, const uint2* __restrict__ tw, u32 q, u32* sm, int tl,
-                     Addr addr, Sync sync) {
+template <int LP, int BIN, class TW, class Addr, class Sync>
+LF_DEV void fwd_line(u32* x, u32 root, const TW& tw, u32 q, u32* sm, int tl, Addr addr,
+                     Sync sync) {
   using C = LineCfg<LP>;
-  ct_sub<C::LA, BIN>(x, root, tw, q);
+  ct_sub<C::LA, BIN, 0>(x, root, tw, q);
   xchg_12<LP>(x, sm, tl, addr, sync);
   constexpr int B1 = FwdLineBound<LP, BIN>::step1;
 #pragma unroll
   for (int gi = 0; gi < C::G; ++gi)
-    ct_sub<C::LB, B1>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
+    ct_sub<C::LB, B1, C::LA>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
+}
+template <int LP, int BIN, class Addr, class Sync>
+LF_DEV void fwd_line(u32* x, u32 root, const uint2* tw, u32 q, u32* sm, int tl, Addr addr,
+                     Sync sync) {
+  fwd_line<LP, BIN>(x, root, TwGlobal{tw}, q, sm, tl, addr, sync);
 }
 
 // Inverse line: x in step-2 layout ([0,2q)) -> step-1 layout ([0,2q)), no N^-1 scaling.
-template <int LP, class Addr, class Sync>
-LF_DEV void inv_line(u32* x, u32 root, const uint2* __restrict__ tw, u32 q, u32* sm, int tl,
-                     Addr addr, Sync sync) {
+template <int LP, class TW, class Addr, class Sync>
+LF_DEV void inv_line(u32* x, u32 root, const TW& tw, u32 q, u32* sm, int tl, Addr addr,
+                     Sync sync) {
   using C = LineCfg<LP>;
 #pragma unroll
   for (int gi = 0; gi < C::G; ++gi)
-    gs_sub<C::LB>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
+    gs_sub<C::LB, C::LA>(x + gi * C::T, (root << C::LA) + tl * C::G + gi, tw, q);
   xchg_21<LP>(x, sm, tl, addr, sync);
-  gs_sub<C::LA>(x, root, tw, q);
+  gs_sub<C::LA, 0>(x, root, tw, q);
+}
+template <int LP, class Addr, class Sync>
+LF_DEV void inv_line(u32* x, u32 root, const uint2* tw, u32 q, u32* sm, int tl, Addr addr,
+                     Sync sync) {
+  inv_line<LP>(x, root, TwGlobal{tw}, q, sm, tl, addr, sync);
 }

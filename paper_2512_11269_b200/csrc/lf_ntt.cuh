@@ -42,7 +42,8 @@ struct NttShape {
   // kernels whose CTA works on lines of ONE row (all lines share a prime): at most 2^L1 lines
   static constexpr int LPCR = LPC < (1 << L1) ? LPC : (1 << L1);
   static constexpr int TRR = TR_LINE * LPCR;
-  static constexpr int FWD_C_OUT = FwdLineBound<L1, 1>::value;             // bound after pass C
+  // bound after any column pass (the BConv kernels feed it lazily reduced inputs < 4q)
+  static constexpr int FWD_C_OUT = FwdLineBound<L1, 4>::value;
 };
 
 // ---- column pass loads/stores (thread (tl, c) of a CW-column tile) ----------------------
@@ -131,3 +132,15 @@ LF_DEV void store_row_step2(const u32* x, u32* base, int tl) {
     case 16: FN(8, 8); break;                      \
     default: lf_set_error("unsupported logN %d", logN); return 2; \
   }
+
+// Shared memory of a row-pass CTA (LPCR lines of one row): staged twiddle subtrees
+// (LPCR * (2^L2 - 1) uint2), then per line the exchange buffer plus `extra` words.
+template <int L1, int L2>
+inline size_t rowpass_smem_bytes(int extra) {
+  using S = NttShape<L1, L2>;
+  return ((size_t)2 * S::LPCR * (LineCfg<L2>::M - 1) + 2 + (size_t)S::LPCR * (pitchR<L2>() + extra)) * 4;
+}
+template <int L1, int L2>
+LF_DEV u32* rowpass_xs(u32* sm) {
+  return sm + 2 * NttShape<L1, L2>::LPCR * (LineCfg<L2>::M - 1) + 2;
+}
