@@ -122,6 +122,15 @@ int lf_rotate(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstrid
               const uint32_t* key, size_t key_bstride, uint32_t* out, size_t out_bstride,
               int batch, void* workspace, void* stream);
 
+/* Hoisted rotations (the reference's hoisting semantics, ckks.py:1-7, 197-203 and
+ * polyir.py:435-469): ONE ModUp of ct.a shared by n_rot Galois automorphisms gs[r] with keys
+ * keys[r] (host array of device pointers).  out: n_rot ciphertexts, out_bstride words apart.
+ * Bit-identical to n_rot separate lf_rotate calls. */
+size_t lf_rotate_hoisted_workspace_bytes(const lf_ctx* ctx, int level, int n_rot);
+int lf_rotate_hoisted(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                      const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                      size_t out_bstride, void* workspace, void* stream);
+
 /* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,

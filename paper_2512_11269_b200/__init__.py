@@ -11,7 +11,7 @@ from .encoding import Plaintext, decode, encode
 from .keys import (EvalKey, PublicKey, SecretKey, keygen, make_conjugation_key, make_galois_key,
                    make_rotation_key)
 from .ckks import (Ciphertext, add_plain, apply_galois, decrypt, encrypt, hom_add, hom_conjugate,
-                   hom_mul, hom_rotate, hom_sub, keyswitch, keyswitch_decompose,
+                   hom_mul, hom_rotate, hom_rotate_hoisted, hom_sub, keyswitch, keyswitch_decompose,
                    keyswitch_inner_product, mul_plain, rescale)
 
 __all__ = [
@@ -21,7 +21,7 @@ __all__ = [
     "make_galois_key",
     "Ciphertext", "add_plain", "decrypt", "encrypt", "hom_add", "hom_mul", "hom_rotate",
     "hom_sub", "mul_plain", "rescale", "keyswitch", "keyswitch_decompose",
-    "keyswitch_inner_product", "apply_galois", "hom_conjugate",
+    "keyswitch_inner_product", "apply_galois", "hom_conjugate", "hom_rotate_hoisted",
     "Domain", "RnsPolynomial",
 ]
 

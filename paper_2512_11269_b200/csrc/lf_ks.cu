@@ -22,6 +22,7 @@
 #include "lf_ops.h"
 
 #define LF_BC_MAXG 16
+#define LF_MAXB 64     // batch instances per launch (per-instance key / galois element)
 
 // Bulk L2 prefetch (TMA engine, sm_90+): warms the next stage's contiguous row segment so the
 // per-thread loads that follow hit L2 instead of HBM.  bytes must be a multiple of 16.
@@ -284,14 +285,14 @@ struct KsInnerArgs {
   const u32* T1;       // beta x ext rows
   const u32* x;        // own rows source (x, or a1 for the tensor mode)
   const u32* x2;       // a2 (tensor mode)
-  const u32* key;      // (d, 2, R, N)
   u32* acc;            // 2 x (l+1) rows
   u32* T2;             // 2 x alpha rows
-  size_t t1_bs, x_bs, key_bs, acc_bs, t2_bs;
+  size_t t1_bs, x_bs, acc_bs, t2_bs;
   const u32* rowk;     // plan: per main row {s, s', pinv, pinv'}
   int level, d, beta, L, alpha, R;
-  u32 g;               // galois element (GALOIS mode)
   int nbatch;          // grid.x = batch (fastest, so a key line is reused from L2) x lines
+  const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
+  u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
 };
 
 template <int L1, int L2, bool GALOIS, int XMODE>
@@ -319,13 +320,15 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   const AddrR<L2> addr{0};
 
   int hs = hi;
-  if (GALOIS) hs = (int)(auto_src_index((u32)hi << L2, A.g, logN) >> L2);
+  const u32 gal = A.gs[b];
+  const u32* keyb = A.keyp[b];
+  if (GALOIS) hs = (int)(auto_src_index((u32)hi << L2, gal, logN) >> L2);
   // twiddle subtrees of this CTA's source lines.  The automorphism maps an aligned block of
   // LPCR lines onto an aligned block of LPCR lines, so one staged block serves all of them.
   uint2* tws = reinterpret_cast<uint2*>(sm);
   int hi0s = (bl % groups) * S::LPCR;
   if (GALOIS)
-    hi0s = (int)((auto_src_index((u32)hi0s << L2, A.g, logN) >> L2) / S::LPCR) * S::LPCR;
+    hi0s = (int)((auto_src_index((u32)hi0s << L2, gal, logN) >> L2) / S::LPCR) * S::LPCR;
   stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
                        threadIdx.x, blockDim.x);
   cp_async_wait_all();
@@ -342,17 +345,15 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       const size_t lo0 = (size_t)hi0 << L2;
       if (!(is_main && (t % A.d) == j))
         prefetch_l2(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + lo0, SEG * 4);
-      prefetch_l2(A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo0, SEG * 4);
-      prefetch_l2(A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo0, SEG * 4);
+      prefetch_l2(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo0, SEG * 4);
+      prefetch_l2(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo0, SEG * 4);
     }
   };
   (void)prefetch_digit;
   for (int j = 0; j < A.beta; ++j) {
     u32 kvb[C::E], kva[C::E];
-    load_row_step2<L2>(kvb, A.key + b * A.key_bs + (((size_t)(j * 2 + 0) * A.R + pi) << logN) +
-                                ((size_t)hi << L2), tl);
-    load_row_step2<L2>(kva, A.key + b * A.key_bs + (((size_t)(j * 2 + 1) * A.R + pi) << logN) +
-                                ((size_t)hi << L2), tl);
+    load_row_step2<L2>(kvb, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
+    load_row_step2<L2>(kva, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
     u32 pc[C::E];
     if (is_main && (t % A.d) == j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
@@ -362,7 +363,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e) {
         const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-        const u32 src = GALOIS ? auto_src_index(pos, A.g, logN) : pos;
+        const u32 src = GALOIS ? auto_src_index(pos, gal, logN) : pos;
         u32 v = xr[src];
         if (XMODE == 1) v = mulmod(v, xr2[src], pk);
         pc[e] = mul_shoup_lazy(v, s, sp, pk.q);
@@ -379,7 +380,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-          pc[e] = perm_buf[auto_src_index(pos, A.g, logN) & (M2 - 1)];
+          pc[e] = perm_buf[auto_src_index(pos, gal, logN) & (M2 - 1)];
         }
       }
     }
@@ -423,7 +424,7 @@ struct ModDownArgs {
   const u32* scal;     // per target t: scalar, Shoup companion at scal[t*sstride], +1
   int sstride;
   int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
-  u32 g;
+  u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
 };
 
 template <int L1, int L2, int EPI>
@@ -490,7 +491,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-          av[e] = addmod(av[e], br[auto_src_index(pos, A.g, logN)], pk.q);
+          av[e] = addmod(av[e], br[auto_src_index(pos, A.gs[b], logN)], pk.q);
         }
       }
     }
@@ -537,28 +538,39 @@ k_pieces(const u32* __restrict__ T1, const u32* __restrict__ x, u32* __restrict_
 // host side
 struct KsWs {
   u32 *T0, *T1, *acc, *T2, *T3;
-  size_t per;    // words per batch instance
+  size_t per_sh;   // words per instance of the shared part (ModUp output), 0 when hoisted
+  size_t per;      // words per instance of the per-key part
 };
 
-static size_t ks_ws_rows(const LfKsPlan* P, int level) {
+static size_t ks_ws_rows_shared(const LfKsPlan* P, int level) {
   const int l1 = level + 1, ext = l1 + P->n_special;
   const int beta = P->d < l1 ? P->d : l1;
-  return (size_t)l1 + (size_t)beta * ext + 2 * (size_t)l1 + 2 * (size_t)P->n_special + 2 * (size_t)l1;
+  return (size_t)l1 + (size_t)beta * ext;
+}
+static size_t ks_ws_rows_inst(const LfKsPlan* P, int level) {
+  const int l1 = level + 1;
+  return 4 * (size_t)l1 + 2 * (size_t)P->n_special;
+}
+static size_t ks_ws_rows(const LfKsPlan* P, int level) {
+  return ks_ws_rows_shared(P, level) + ks_ws_rows_inst(P, level);
 }
 
-static KsWs carve(const LfCtx* ctx, int level, void* ws) {
+// Layout: nsh x [T0 | T1] then batch x [acc | T2 | T3].
+static KsWs carve(const LfCtx* ctx, int level, void* ws, int nsh = 1, bool hoisted = false) {
   const LfKsPlan* P = ctx->ks;
-  const int l1 = level + 1, ext = l1 + P->n_special;
-  const int beta = P->d < l1 ? P->d : l1;
+  const int l1 = level + 1;
   const size_t N = ctx->N;
+  const size_t sh = ks_ws_rows_shared(P, level) * N, in = ks_ws_rows_inst(P, level) * N;
   KsWs w;
   u32* p = (u32*)ws;
-  w.T0 = p; p += (size_t)l1 * N;
-  w.T1 = p; p += (size_t)beta * ext * N;
-  w.acc = p; p += 2 * (size_t)l1 * N;
-  w.T2 = p; p += 2 * (size_t)P->n_special * N;
-  w.T3 = p; p += 2 * (size_t)l1 * N;
-  w.per = ks_ws_rows(P, level) * N;
+  w.T0 = p;
+  w.T1 = p + (size_t)l1 * N;
+  p += (size_t)nsh * sh;
+  w.acc = p;
+  w.T2 = p + 2 * (size_t)l1 * N;
+  w.T3 = w.T2 + 2 * (size_t)P->n_special * N;
+  w.per_sh = hoisted ? 0 : sh;
+  w.per = in;
   return w;
 }
 
@@ -598,15 +610,21 @@ enum { OP_KS = 0, OP_MUL = 1, OP_ROT = 2 };
 
 struct KsCall {
   int level, batch, op;
+  bool hoisted;             // one ModUp shared by all instances (x_bs = e_bs = 0)
   const u32 *x, *x2;        // K_A/K_C inputs: x (op KS: the poly; MUL: a1, a2; ROT: ct.a)
   size_t x_bs;
-  const u32* key;
+  const u32* key;           // instance b uses keylist[b0+b] if given, else key + (b0+b)*key_bs
   size_t key_bs;
+  const u32* const* keylist;
   u32* out;                 // batch x 2 x (l+1)
   size_t out_bs;
   const u32 *e0, *e1;       // epilogue (MUL: ct1, ct2; ROT: ct)
   size_t e_bs;
-  u32 g;
+  u32 g;                    // galois element (ROT): glist[b0+b] if given, else g
+  const u32* glist;
+  int b0;                   // first instance of this chunk
+  const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
+  u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
 
 template <int L1, int L2>
@@ -617,7 +635,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   const KsLevelPlan& K = P->lv[c.level];
   const int l1 = c.level + 1, alpha = P->n_special;
   const size_t N = ctx->N;
-  const KsWs w = carve(ctx, c.level, ws);
+  const int nsh = c.hoisted ? 1 : c.batch;
+  const KsWs w = carve(ctx, c.level, ws, nsh, c.hoisted);
   const LfDev dv = ctx->dev();
   const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
@@ -626,18 +645,18 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   LF_MARK(0);
   // K_A
   {
-    dim3 grid(l1 * groups, 1, c.batch);
+    dim3 grid(l1 * groups, 1, nsh);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, 1, 0, -1); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per, l1, dv, 1, 0, -1); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, 1, 0, -1); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
   // K_BC (ModUp)
   {
     BcArgs A{};
-    A.src = w.T0; A.dst = w.T1; A.src_bs = w.per; A.dst_bs = w.per;
+    A.src = w.T0; A.dst = w.T1; A.src_bs = w.per_sh; A.dst_bs = w.per_sh;
     A.ngroups = K.beta;
     int kmax = 0, mmax = 0;
     for (int j = 0; j < K.beta; ++j) {
@@ -645,17 +664,18 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
       kmax = K.up[j].B.k > kmax ? K.up[j].B.k : kmax;
       mmax = K.up[j].B.m > mmax ? K.up[j].B.m : mmax;
     }
-    A.tsplit = bc_tsplit(K.beta, c.batch, (1 << L2) / 8, mmax);
-    if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, kmax, s)) return e;
+    A.tsplit = bc_tsplit(K.beta, nsh, (1 << L2) / 8, mmax);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, nsh, kmax, s)) return e;
   }
   LF_MARK(2);
   // K_C
   {
     KsInnerArgs A{};
-    A.T1 = w.T1; A.x = c.x; A.x2 = c.x2; A.key = c.key; A.acc = w.acc; A.T2 = w.T2;
-    A.t1_bs = w.per; A.x_bs = c.x_bs; A.key_bs = c.key_bs; A.acc_bs = w.per; A.t2_bs = w.per;
+    A.T1 = w.T1; A.x = c.x; A.x2 = c.x2; A.acc = w.acc; A.T2 = w.T2;
+    A.t1_bs = w.per_sh; A.x_bs = c.x_bs; A.acc_bs = w.per; A.t2_bs = w.per;
     A.rowk = P->rowk; A.level = c.level; A.d = P->d; A.beta = K.beta; A.L = P->L; A.alpha = alpha;
-    A.R = P->L + 1 + alpha; A.g = c.g; A.nbatch = c.batch;
+    A.R = P->L + 1 + alpha; A.nbatch = c.batch;
+    for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
     const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
     dim3 grid(K.ext * groups * c.batch);
     if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv); }
@@ -686,7 +706,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     ModDownArgs A{};
     A.T3 = w.T3; A.acc = w.acc; A.out = c.out; A.e0 = c.e0; A.e1 = c.e1;
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
-    A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1; A.g = c.g;
+    A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1;
+    for (int b = 0; b < c.batch; ++b) A.gs[b] = c.g_of(b);
     dim3 grid(l1 * groups, 1, c.batch);
     if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); k_moddown_out<L1, L2, EPI_MUL><<<grid, S::TRR, smR, s>>>(A, dv); }
     else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); k_moddown_out<L1, L2, EPI_ROT><<<grid, S::TRR, smR, s>>>(A, dv); }
@@ -732,7 +753,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, const u32* ct, size_t c
     A.T3 = T3; A.acc = ct; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
     A.t3_bs = per; A.acc_bs = ct_bs; A.out_bs = out_bs; A.e_bs = 0;
     A.scal = P->qinv + (size_t)l * P->n_main * 2; A.sstride = 2;
-    A.nt = l; A.nacc = l + 1; A.ne = 0; A.g = 0;
+    A.nt = l; A.nacc = l + 1; A.ne = 0;
     dim3 grid(l * groups, 1, batch);
     { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
@@ -787,11 +808,31 @@ static int ks_check(const lf_ctx* ctx, int level) {
   return 0;
 }
 
-static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
-                  cudaEvent_t* ev = nullptr) {
+static int run_ks_chunk(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
+                        cudaEvent_t* ev) {
 #define LF_KS(A, B) { if (int e = ks_pipeline<A, B>(ctx, c, ws, s, ev)) return e; }
   LF_DISPATCH_LOGN(ctx->logN, LF_KS)
 #undef LF_KS
+  return 0;
+}
+
+// Instances are processed LF_MAXB at a time (the per-instance key / galois tables live in the
+// kernel parameters); the workspace of a chunk is reused by the next one on the same stream.
+static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
+                  cudaEvent_t* ev = nullptr) {
+  if (c.batch <= LF_MAXB) return run_ks_chunk(ctx, c, ws, s, ev);
+  if (ev) { lf_set_error("profiled keyswitch: batch > %d", LF_MAXB); return 2; }
+  for (int b0 = 0; b0 < c.batch; b0 += LF_MAXB) {
+    KsCall k = c;
+    k.batch = c.batch - b0 < LF_MAXB ? c.batch - b0 : LF_MAXB;
+    k.x = c.x + (c.hoisted ? 0 : b0 * c.x_bs);
+    if (c.x2) k.x2 = c.x2 + (c.hoisted ? 0 : b0 * c.x_bs);
+    k.out = c.out + b0 * c.out_bs;
+    if (c.e0) k.e0 = c.e0 + (c.hoisted ? 0 : b0 * c.e_bs);
+    if (c.e1) k.e1 = c.e1 + (c.hoisted ? 0 : b0 * c.e_bs);
+    k.b0 = b0;
+    if (int e = run_ks_chunk(ctx, k, ws, s, nullptr)) return e;
+  }
   return 0;
 }
 
@@ -866,6 +907,32 @@ int lf_keyswitch_profiled(const lf_ctx* ctx, int level, const uint32_t* x, size_
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
+}
+
+size_t lf_rotate_hoisted_workspace_bytes(const lf_ctx* ctx, int level, int n_rot) {
+  if (ks_check(ctx, level)) return 0;
+  const int n = n_rot < LF_MAXB ? (n_rot < 1 ? 1 : n_rot) : LF_MAXB;
+  return (ks_ws_rows_shared(ctx->ks, level) + (size_t)n * ks_ws_rows_inst(ctx->ks, level)) *
+         (size_t)ctx->N * 4;
+}
+
+int lf_rotate_hoisted(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                      const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                      size_t out_bstride, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct || !gs || !keys || !out || !workspace || n_rot < 1) {
+    lf_set_error("lf_rotate_hoisted: bad argument");
+    return 1;
+  }
+  for (int r = 0; r < n_rot; ++r)
+    if (!(gs[r] & 1) || !keys[r]) { lf_set_error("lf_rotate_hoisted: rotation %d: bad key or even galois element", r); return 2; }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = n_rot; c.op = OP_ROT; c.hoisted = true;
+  c.x = ct + arow; c.x2 = c.x; c.x_bs = 0; c.keylist = keys;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct; c.e1 = nullptr; c.e_bs = 0;
+  c.glist = gs;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
 }
 
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch) {

@@ -182,3 +182,38 @@ def test_c2_matches_reference(B, golden_params, level):
     assert digest(_pack(B.hom_rotate(ct1, 1, rk1, p))) == m["rot1"]
     assert digest(_pack(B.hom_mul(ct1, ct2, rlk, p))) == m["mul"]
     assert digest(_pack(B.rescale(ct1, p))) == m["rescale"]
+
+
+@pytest.mark.parametrize("name", ["desk", "n1024"])
+def test_hoisted_rotations_bit_identical(B, golden_params, name):
+    """One shared ModUp for several rotations == separate hom_rotate calls (the reference's
+    hoisting contract, tests/test_polyir.py:257-265), including conjugation."""
+    kw = dict(golden_params[name]["kwargs"])
+    p = B.gen_params(**kw)
+    sk, pk, rlk = B.keygen(p, seed=3)
+    steps = [1, 2, 5, p.n - 1, 0, 7]
+    keys = {s: B.make_rotation_key(p, sk, s, np.random.default_rng(10 + s)) for s in steps if s % p.n}
+    v = np.random.default_rng(4).uniform(-1, 1, p.n)
+    for level in (p.max_level, 2):
+        ct = B.encrypt(B.encode(v, p, level=level), pk, p, np.random.default_rng(level))
+        got = B.hom_rotate_hoisted(ct, steps, keys, p)
+        for s, g in zip(steps, got):
+            want = B.hom_rotate(ct, s, keys.get(s % p.n), p)
+            assert np.array_equal(_pack(g), _pack(want)), (level, s)
+    dec = B.decrypt(got[0], sk, p)
+    assert np.abs(dec - np.roll(v, -1)).max() < 0.05
+
+
+def test_batched_keyswitch_matches_single(B, golden_params):
+    from paper_2512_11269_b200 import fused
+    p = B.gen_params(**golden_params["desk"]["kwargs"])
+    sk, pk, rlk = B.keygen(p, seed=3)
+    import torch
+    l1 = p.max_level + 1
+    q = torch.tensor(p.rns_basis, dtype=torch.int64, device="cuda")[:, None]
+    xs = (torch.randint(0, 2 ** 62, (70, l1, p.N), device="cuda", dtype=torch.int64) % q).to(torch.int32)
+    out = fused.keyswitch_batch(p, p.max_level, xs, rlk)      # > LF_MAXB: chunked
+    for i in (0, 37, 69):
+        kb, ka = B.keyswitch(B.RnsPolynomial(xs[i], B.Domain.EVAL, tuple(range(l1))), rlk, p)
+        assert np.array_equal(out[i, 0].cpu().numpy(), kb.limbs.cpu().numpy())
+        assert np.array_equal(out[i, 1].cpu().numpy(), ka.limbs.cpu().numpy())
