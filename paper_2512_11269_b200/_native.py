@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcerium_b200.so")
+LIB_PATH = os.environ.get("LF_LIB_PATH") or os.path.join(_HERE, "libcerium_b200.so")
 
 _u32p = ctypes.c_void_p          # device pointers are passed as raw addresses
 _i32_host = ctypes.POINTER(ctypes.c_int32)

@@ -145,9 +145,62 @@ LF_DEV u32 reduce64_lazy4(u64 x, const PrimeK& k) {
   return mul_shoup_lazy(hi, k.r32, k.r32p, k.q) + reduce32_lazy(lo, k);
 }
 
+// Multiply-accumulate of one target over the K source tiles of this thread, for the EH
+// positions [h*EH, (h+1)*EH) of its E: acc[j] += y_i[j] * w[i] (64-bit lazy sums, exact:
+// K * 2^56 < 2^64).  KEX > 0: K known at compile time (fully unrolled, weights in registers);
+// KEX == 0: runtime K, one source per iteration with the next weight prefetched.
+template <int E, int EH, int KEX, int YI>
+LF_DEV void bconv_mac(u64* acc, const u32* const* yq, const u32* wv_pre,
+                      const u32* __restrict__ wt, int k, const u32* slot0, int h) {
+  if constexpr (E % 16 == 0) {
+    if constexpr (KEX > 0) {
+#pragma unroll
+      for (int i = 0; i < KEX; ++i) {
+#pragma unroll
+        for (int q = 0; q < EH / 4; ++q) {
+          const int lq = h * (EH / 4) + q;
+          const uint4 tv = *reinterpret_cast<const uint4*>(yq[lq & 3] + i * YI + 16 * (lq >> 2));
+          acc[4 * q + 0] += (u64)tv.x * wv_pre[i];
+          acc[4 * q + 1] += (u64)tv.y * wv_pre[i];
+          acc[4 * q + 2] += (u64)tv.z * wv_pre[i];
+          acc[4 * q + 3] += (u64)tv.w * wv_pre[i];
+        }
+      }
+    } else {
+      u32 wn = __ldg(&wt[0]);
+#pragma unroll 1
+      for (int i = 0; i < k; ++i) {
+        const u32 wv = wn;
+        if (i + 1 < k) wn = __ldg(&wt[i + 1]);
+#pragma unroll
+        for (int q = 0; q < EH / 4; ++q) {
+          const int lq = h * (EH / 4) + q;
+          const uint4 tv = *reinterpret_cast<const uint4*>(yq[lq & 3] + i * YI + 16 * (lq >> 2));
+          acc[4 * q + 0] += (u64)tv.x * wv;
+          acc[4 * q + 1] += (u64)tv.y * wv;
+          acc[4 * q + 2] += (u64)tv.z * wv;
+          acc[4 * q + 3] += (u64)tv.w * wv;
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < k; ++i) {
+      const u32 wv = __ldg(&wt[i]);
+      const u32* slot = slot0 + (size_t)i * YI + h * EH;
+#pragma unroll
+      for (int j = 0; j < EH; ++j) acc[j] += (u64)slot[j] * wv;
+    }
+  }
+}
+
 // grid.x = batch (fastest) x column tiles x (groups * tsplit); TG thread groups share the tile.
-template <int L1, int L2, int CW, int KMAX, int TG>
-__global__ void __launch_bounds__(TG * CW * LineCfg<L1>::T, (TG * CW * LineCfg<L1>::T) >= 512 ? 2 : 1)
+// KEX > 0: every group of the launch has exactly KEX sources (compile-time unrolled MACs).
+#ifndef LF_BC_MINB
+#define LF_BC_MINB 2
+#endif
+template <int L1, int L2, int CW, int KMAX, int TG, int KEX>
+__global__ void __launch_bounds__(TG * CW * LineCfg<L1>::T, (TG * CW * LineCfg<L1>::T) >= 512 ? LF_BC_MINB : 1)
 k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   using C = LineCfg<L1>;
   constexpr int E = C::E, T = C::T;
@@ -155,7 +208,6 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   constexpr int NCT = (1 << L2) / CW;
   constexpr int logN = L1 + L2;
   constexpr int YI = T * CW * E;                               // words per source
-  constexpr int EH = E >= 16 ? E / 2 : E;                      // MAC in halves (registers)
   extern __shared__ __align__(16) u32 sm[];
   const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
   const int c = lt % CW, tl = lt / CW;
@@ -168,7 +220,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const BcGroupDev& G = A.g[gy / A.tsplit];
   const int ts = gy % A.tsplit;
   const BconvDev& B = G.B;
-  const int k = B.k;
+  const int k = KEX > 0 ? KEX : B.k;
   const int col = ct * CW + c;
   u32* Ybase = sm + (size_t)(tl * CW + c) * E;
   u32* X = sm + (size_t)kmax * YI + grp * smemC_words<L1, CW>();
@@ -199,15 +251,13 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     double v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) v[j] = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < k; ++i) {
+      u32 y[E];
+      y_load<E>(y, Ybase + (size_t)i * YI, rot);
+      const double is = B.inv_s[i];
 #pragma unroll
-    for (int i = 0; i < KMAX; ++i) {
-      if (i < k) {
-        u32 y[E];
-        y_load<E>(y, Ybase + (size_t)i * YI, rot);
-        const double is = B.inv_s[i];
-#pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = fma((double)y[j], is, v[j]);
-      }
+      for (int j = 0; j < E; ++j) v[j] = fma((double)y[j], is, v[j]);
     }
 #pragma unroll
     for (int w = 0; w < (E + 3) / 4; ++w) up[w] = 0;
@@ -237,11 +287,18 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   for (int q = 0; q < 4; ++q) yq[q] = Ybase + 4 * ((q + rot) & 3);
   const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
+#pragma unroll 1
   for (int t = t0 + grp; t < t1; t += TG) {
     const int pi = B.tgt_pi[t];
     const PrimeK pk = dv.pk[pi];
-    const u32* wt = B.w + (size_t)t * k;
     const u32 ns = B.negS[t];
+    const u32* wt = B.w + (size_t)t * k;
+    u32 wv_pre[KEX > 0 ? KEX : 1];
+    if constexpr (KEX > 0) {
+#pragma unroll
+      for (int i = 0; i < KEX; ++i) wv_pre[i] = __ldg(&wt[i]);
+    }
+    constexpr int EH = E >= 16 ? E / 2 : E;
     u32 x[E];
 #pragma unroll
     for (int h = 0; h < E / EH; ++h) {
@@ -249,27 +306,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 #pragma unroll
       for (int j = 0; j < EH; ++j)
         acc[j] = (u64)((up[(h * EH + j) / 4] >> (8 * ((h * EH + j) % 4))) & 0xFFu) * ns;
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i) {
-        if (i < k) {
-          const u32 wv = __ldg(&wt[i]);
-          const u32* slot = Ybase + (size_t)i * YI;
-          u32 y[EH];
-          if constexpr (E % 16 == 0) {
-#pragma unroll
-            for (int q = 0; q < EH / 4; ++q) {
-              const int lq = h * (EH / 4) + q;
-              const uint4 tv = *reinterpret_cast<const uint4*>(yq[lq & 3] + (size_t)i * YI + 16 * (lq >> 2));
-              y[4 * q] = tv.x; y[4 * q + 1] = tv.y; y[4 * q + 2] = tv.z; y[4 * q + 3] = tv.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < EH; ++j) y[j] = slot[h * EH + j];
-          }
-#pragma unroll
-          for (int j = 0; j < EH; ++j) acc[j] += (u64)y[j] * wv;
-        }
-      }
+      bconv_mac<E, EH, KEX, YI>(acc, yq, wv_pre, wt, k, Ybase, h);
 #pragma unroll
       for (int j = 0; j < EH; ++j) x[h * EH + j] = reduce64_lazy4(acc[j], pk);
     }
@@ -574,12 +611,12 @@ static KsWs carve(const LfCtx* ctx, int level, void* ws, int nsh = 1, bool hoist
   return w;
 }
 
-template <int L1, int L2, int CW, int KMAX, int TG>
+template <int L1, int L2, int CW, int KMAX, int TG, int KEX>
 static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   using Y_ = YTile<L1>;
   const size_t sm = ((size_t)kmax * Y_::T * CW * Y_::E + (size_t)TG * smemC_words<L1, CW>()) * 4;
   if (sm > 227 * 1024) { lf_set_error("bconv: shared memory %zu too large", sm); return 2; }
-  auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG>;
+  auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG, KEX>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const long nblocks = (long)batch * ((1 << L2) / CW) * A.ngroups * A.tsplit;
   kern<<<(unsigned)nblocks, TG * CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax, batch);
@@ -587,16 +624,29 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
   return 0;
 }
 
-// Column tile width and group count: CW = 8 columns (32-byte row segments) and two thread
+// Column tile width and group count: CW = 8 columns (32-byte row segments) and four thread
 // groups sharing the source tile for the production sizes; narrower tiles for large digit
-// counts (d = 1 style parameter sets) or tiny rings.
+// counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches whose groups all
+// have the same source count 1..9 use the compile-time-K kernel.
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   constexpr int NCOL = 1 << L2;
   constexpr int CW8 = NCOL >= 8 ? 8 : NCOL;
   constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 4 : 1;
-  if (kmax <= 16) return launch_bc<L1, L2, CW8, 16, TG>(ctx, A, batch, kmax, s);
-  return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1), 64, 1>(ctx, A, batch, kmax, s);
+  if (kmax > 16) return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1), 64, 1, 0>(ctx, A, batch, kmax, s);
+  if constexpr (L1 == 8 && L2 == 8) {
+    bool uniform = true;
+    for (int g = 0; g < A.ngroups; ++g) uniform &= A.g[g].B.k == kmax;
+    if (uniform) {
+      switch (kmax) {
+#define LF_BC_K(K) case K: return launch_bc<L1, L2, CW8, 16, TG, K>(ctx, A, batch, kmax, s);
+        LF_BC_K(1) LF_BC_K(2) LF_BC_K(3) LF_BC_K(4) LF_BC_K(5) LF_BC_K(6) LF_BC_K(7) LF_BC_K(8) LF_BC_K(9)
+#undef LF_BC_K
+        default: break;
+      }
+    }
+  }
+  return launch_bc<L1, L2, CW8, 16, TG, 0>(ctx, A, batch, kmax, s);
 }
 
 static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax) {
