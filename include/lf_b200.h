@@ -42,6 +42,7 @@ typedef struct LfCtx lf_ctx;
 #define LF_OP_MULACC 5         /* c + a * b             row_mulacc   poly.py:98   */
 #define LF_OP_MODSTEP 6        /* (a - b) * s_r         row_modstep  poly.py:112  */
 #define LF_OP_MUL_SCALAR_ADD 7 /* a * s_r + b           (fused helper)            */
+#define LF_OP_ADD_SCALAR 8     /* a + s_r               (constant add, bootstrap)  */
 
 int lf_abi_version(void);
 const char* lf_last_error(void);
@@ -140,6 +141,21 @@ int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstri
  * eval domain, digit-major; beta = min(d, level+1).  Workspace as lf_keyswitch (batch 1). */
 int lf_ks_decompose(const lf_ctx* ctx, int level, const uint32_t* x, uint32_t* pieces,
                     void* workspace, void* stream);
+
+/* ---- bootstrap helpers (no reference counterpart: the reference has no bootstrap,
+ * SPEC.md:8,136; built from the reference's row primitives, poly.py:85-121) ------------- */
+
+/* ModRaise: `in` holds nin coefficient-domain rows mod q_0 (prime index 0); out receives
+ * nin x nout rows, row i*nout + r = centred lift of in[i] (in (-q0/2, q0/2]) mod prime r. */
+int lf_modraise(const lf_ctx* ctx, uint32_t* out, const uint32_t* in, int nin, int nout,
+                void* stream);
+
+/* Plaintext multiply-accumulate of a linear transform: out (2 x nrows rows: b then a) =
+ * sum_i (b_i, a_i) * pt_i over nterm <= 32 terms; b, a, pt are HOST arrays of device row
+ * pointers (nrows rows each, main primes 0..nrows-1).  Equals mul_plain + hom_add
+ * (ckks.py:152-179) term by term. */
+int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+             const uint32_t* const* a, const uint32_t* const* pt, void* stream);
 
 #ifdef __cplusplus
 }

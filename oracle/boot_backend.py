@@ -1,0 +1,114 @@
+"""CPU oracle backend of the bootstrap composition — TEST INFRASTRUCTURE ONLY.
+
+`paper_2512_11269_b200.bootstrap.Bootstrapper` is written against a small backend interface.
+This backend implements it with the oracle restatement of the reference primitives
+(oracle/lf_oracle.py: hom_rotate ckks.py:197-217, mul_plain/hom_add/hom_sub ckks.py:152-179,
+hom_mul ckks.py:182-194, rescale ckks.py:220-225, p_scale poly.py:204-209) plus the two
+bootstrap-only helpers restated in numpy (ModRaise, constant add), so that the GPU bootstrap
+can be checked residue for residue against the same composition on the CPU.
+Only tests/ may import this module.
+"""
+
+from fractions import Fraction
+
+import numpy as np
+
+from . import lf_oracle as O
+
+U64 = np.uint64
+
+
+def encode_ints(values, N, scale):
+    r = np.rint(O.embed_inverse(np.asarray(values, dtype=np.complex128), N) * float(scale))
+    return r.astype(np.int64)
+
+
+def monomial_ints(N, e):
+    c = np.zeros(N, dtype=np.int64)
+    e %= 2 * N
+    c[e % N] = -1 if e >= N else 1
+    return c
+
+
+class OracleBackend:
+    def __init__(self, P: O.Params, rlk, ck, rk: dict):
+        self.P = P
+        self.N = P.N
+        self.main_primes = tuple(P.main)
+        self.default_scale = P.scale
+        self.rlk, self.ck, self.rk = rlk, ck, rk
+        self.calls = []
+
+    def _ids(self, level):
+        return self.P.main_ids(level)
+
+    def drop_to_level(self, ct, level):
+        if ct.level == level:
+            return ct
+        ids = self._ids(level)
+        return O.Ct(O.Poly(ct.b.rows[: level + 1].copy(), ids), O.Poly(ct.a.rows[: level + 1].copy(), ids),
+                    ct.scale, level)
+
+    def mod_raise(self, ct):
+        P = self.P
+        q0 = P.main[0]
+        L = P.L
+        ids = self._ids(L)
+        out = []
+        for poly in (ct.b, ct.a):
+            c = O.ntt_inv(poly.rows[0].copy(), q0).astype(np.int64)
+            c = np.where(c > q0 // 2, c - q0, c)
+            rows = np.stack([O.ntt_fwd(np.mod(c, q).astype(U64), q) for q in P.main])
+            out.append(O.Poly(rows, ids))
+        return O.Ct(out[0], out[1], ct.scale, L)
+
+    def encode_slots(self, values, level, scale):
+        ints = encode_ints(values, self.N, scale)
+        return O.Plain(O.signed_to_eval(self.P, ints, self._ids(level)), Fraction(scale), level)
+
+    def add(self, x, y):
+        assert x.level == y.level and x.scale == y.scale
+        return O.hom_add(self.P, x, y)
+
+    def sub(self, x, y):
+        assert x.level == y.level and x.scale == y.scale
+        return O.hom_sub(self.P, x, y)
+
+    def rescale(self, x):
+        return O.rescale(self.P, x)
+
+    def hom_mul(self, x, y):
+        return O.hom_mul(self.P, x, y, self.rlk)
+
+    def conjugate(self, x):
+        return O.apply_galois(self.P, x, 2 * self.N - 1, self.ck)
+
+    def rotate_hoisted(self, x, steps):
+        return [x if s % self.P.n == 0 else O.hom_rotate(self.P, x, s, self.rk[s % self.P.n]) for s in steps]
+
+    def rotate_many(self, xs, steps):
+        return [x if s % self.P.n == 0 else O.hom_rotate(self.P, x, s, self.rk[s % self.P.n])
+                for x, s in zip(xs, steps)]
+
+    def mul_plain_sum(self, pairs):
+        acc = None
+        for c, pt in pairs:
+            t = O.mul_plain(self.P, c, pt)
+            acc = t if acc is None else O.hom_add(self.P, acc, t)
+        return acc
+
+    def mul_const(self, ct, c, S_p):
+        k = round(Fraction(c) * Fraction(S_p))
+        sc = {b: k % self.P.prime(b) for b in ct.b.ids}
+        return O.Ct(O.p_scale(self.P, ct.b, sc), O.p_scale(self.P, ct.a, sc), ct.scale * Fraction(S_p), ct.level)
+
+    def add_const(self, ct, c):
+        k = round(Fraction(c) * Fraction(ct.scale))
+        q = np.array([self.P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+        kk = np.array([k % self.P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+        b = O.Poly((ct.b.rows + kk) % q, ct.b.ids)
+        return O.Ct(b, ct.a, ct.scale, ct.level)
+
+    def mul_monomial(self, ct, e):
+        m = O.signed_to_eval(self.P, monomial_ints(self.N, e), ct.b.ids)
+        return O.Ct(O.p_mul(self.P, ct.b, m), O.p_mul(self.P, ct.a, m), ct.scale, ct.level)

@@ -61,6 +61,11 @@ def _load():
                                       ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
         "lf_ks_decompose": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, _u32p, ctypes.c_void_p,
                                            ctypes.c_void_p]),
+        "lf_modraise": (ctypes.c_int, [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p]),
+        "lf_ptmac": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

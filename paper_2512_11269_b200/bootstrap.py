@@ -1,0 +1,727 @@
+"""CKKS bootstrapping built from the fused operator API.
+
+The reference has no bootstrap.  This module composes the
+reference's own primitives — hom_rotate (hoisted), mul_plain, hom_add/sub, hom_mul, rescale,
+plus conjugation (a Galois key with g = 2N-1 through keys.py:129-136) — into the standard
+pipeline, so that every primitive call is bit-exact against the reference primitive on the
+same inputs and the whole composition is bit-exact against the CPU oracle composing the
+same calls (tests/test_bootstrap.py).  The algorithm is written once, against a small backend
+interface; `GpuBackend` below is the product (sm_100a kernels through the C ABI), the oracle
+backend lives in oracle/boot_backend.py and is test infrastructure.
+
+Pipeline (input: ciphertext at level 0, modulus q0, any scale Delta_in):
+
+1. ModRaise.  INTT the q0 rows, lift each coefficient centred to (-q0/2, q0/2], reduce into
+   every main prime, NTT (kernel `lf_modraise`).  Decrypts to t = m + e + q0*I with small I
+   (sparse ternary secret, h = 64).
+2. CoeffToSlot.  z = Embed(t)/Delta_in; w = U^-1 z with U_jk = zeta^(5^j k) (the canonical
+   embedding of encoding.py:23-61).  U = F_n ... F_2 BR (radix-2 "special FFT"), so
+   BR U^-1 = F_2^-1 ... F_n^-1: `cts_levels` groups the inverse butterfly stages into
+   `cfg.cts_levels` sparse matrices (<= 2^(r+1)-1 diagonals each) applied with baby-step /
+   giant-step rotations.  Output (bit-reversed order): y_k = c (t_k + i t_{k+n}) / q0.
+   Plaintext diagonals are encoded at the product of the next two primes (q_l q_{l-1}) and
+   the level rescales twice: the input slots are dominated by q0*I, so the diagonals need
+   ~2^-40 relative precision, which a single 26-bit prime cannot give.
+3. Real / imaginary split with one conjugation: re = y + conj(y), im = (y - conj(y)) * (-i)
+   (multiplication by -i is the monomial -X^(N/2), exact).
+4. EvalMod on both parts: u = alpha x + beta maps x = t/q0 in [-K, K] to [-1, 1]; a
+   Chebyshev interpolant of cos(2 pi (x - 1/4) / 2^r) (degree `cheb_degree`, evaluated by
+   recursive Chebyshev division over the powers T_1..T_7, T_8, T_16) followed by r double
+   angles c <- c^2 - s gives sin(2 pi x) / (2 pi) ~= m/q0.  EvalMod runs at scale ~2^52 (two
+   primes per multiplicative level): its absolute noise must stay far below m/q0 ~ 2^-11.
+   Scales are tracked exactly (Fraction) as in the reference; additions of terms that reach
+   a level by different paths are aligned by a multiplication with the constant 1 encoded at
+   the exact compensating scale.
+5. Recombine re + i*im, SlotToCoeff: v = U (bit-reversed input), `cfg.stc_levels` levels,
+   single-prime diagonals, then one final rescale back to a ~2^26 scale.
+
+Precision: see `DESIGN.md` §6 and `bench.py --workload bootstrap` (reported in bits).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+from functools import lru_cache
+from math import ceil, pi
+
+import numpy as np
+
+from .encoding import embed_inverse
+
+# ---------------------------------------------------------------------------------------
+# slot-domain linear algebra (host, complex128)
+#
+# A slot-linear map is stored in diagonal form {offset: vec}: (M z)[p] = sum_d vec_d[p] *
+# z[(p + d) mod n]; rotating a ciphertext by d slots (hom_rotate, "left rotation",
+# ckks.py:197-217) realises z -> z[(p + d) mod n].
+# ---------------------------------------------------------------------------------------
+
+DiagMat = dict
+
+
+def dm_apply(M: DiagMat, z: np.ndarray) -> np.ndarray:
+    out = np.zeros_like(z, dtype=np.complex128)
+    for d, v in M.items():
+        out += v * np.roll(z, -d)
+    return out
+
+
+def dm_compose(A: DiagMat, B: DiagMat, n: int, tol: float = 0.0) -> DiagMat:
+    """A after B: sum_{a,b} diag(alpha_a * rot(beta_b, a)) R^(a+b)."""
+    out = {}
+    for a, va in A.items():
+        for b, vb in B.items():
+            d = (a + b) % n
+            t = va * np.roll(vb, -a)
+            out[d] = out[d] + t if d in out else t
+    return {d: v for d, v in out.items() if np.abs(v).max() > tol}
+
+
+def dm_scale(A: DiagMat, c) -> DiagMat:
+    return {d: v * c for d, v in A.items()}
+
+
+@lru_cache(maxsize=None)
+def _rot_group(N: int):
+    return tuple(pow(5, j, 2 * N) for j in range(N // 2))
+
+
+def _stage(N: int, L: int, inverse: bool) -> DiagMat:
+    """Butterfly stage of block length L of the special FFT (U = F_n ... F_2 BR):
+    (u, v) -> (u + xi v, u - xi v), xi = exp(2 pi i (5^j mod 4L) / 4L) for position j of the
+    half block.  The inverse maps (a, b) -> ((a + b)/2, (a - b)/(2 xi))."""
+    n = N // 2
+    h = L // 2
+    rg = _rot_group(N)
+    p = np.arange(n)
+    j = p % L
+    first = j < h
+    jj = np.where(first, j, j - h)
+    xi = np.exp(2j * np.pi * (np.array(rg, dtype=np.int64)[jj] % (4 * L)) / (4 * L))
+    d0 = np.zeros(n, np.complex128)
+    dp = np.zeros(n, np.complex128)      # offset +h (first half reads p + h)
+    dm = np.zeros(n, np.complex128)      # offset -h (second half reads p - h)
+    if not inverse:
+        d0[first] = 1.0
+        dp[first] = xi[first]
+        dm[~first] = 1.0
+        d0[~first] = -xi[~first]
+    else:
+        # a = out[i+j] (first half), b = out[i+j+h]: u = (a + b)/2 at first, v = (a - b)/(2 xi)
+        d0[first] = 0.5
+        dp[first] = 0.5
+        dm[~first] = 0.5 / xi[~first]
+        d0[~first] = -0.5 / xi[~first]
+    M = {}
+
+    def put(d, v):
+        d %= n
+        M[d] = M[d] + v if d in M else v
+
+    put(0, d0)
+    put(h, dp)
+    put(-h, dm)
+    return M
+
+
+def _groups(nstages: int, nlev: int):
+    """Split nstages consecutive stages into nlev groups, larger groups first."""
+    base, extra = divmod(nstages, nlev)
+    sizes = [base + (1 if i < extra else 0) for i in range(nlev)]
+    return sizes
+
+
+def stc_matrices(N: int, nlev: int) -> list:
+    """SlotToCoeff factors in application order: F_2..F_n grouped into nlev matrices."""
+    n = N // 2
+    logn = n.bit_length() - 1
+    sizes = _groups(logn, nlev)
+    mats, s = [], 1
+    for sz in sizes:
+        M = None
+        for k in range(s, s + sz):
+            F = _stage(N, 1 << k, inverse=False)
+            M = F if M is None else dm_compose(F, M, n)
+        mats.append(M)
+        s += sz
+    return mats
+
+
+def cts_matrices(N: int, nlev: int) -> list:
+    """CoeffToSlot factors in application order: F_n^-1 .. F_2^-1 grouped into nlev
+    matrices (the product equals BR U^-1)."""
+    n = N // 2
+    logn = n.bit_length() - 1
+    sizes = _groups(logn, nlev)
+    mats, s = [], logn
+    for sz in sizes:
+        M = None
+        for k in range(s, s - sz, -1):
+            F = _stage(N, 1 << k, inverse=True)
+            M = F if M is None else dm_compose(F, M, n)
+        mats.append(M)
+        s -= sz
+    return mats
+
+
+def bit_reverse_perm(n: int) -> np.ndarray:
+    bits = n.bit_length() - 1
+    r = np.zeros(n, dtype=np.int64)
+    for i in range(n):
+        r[i] = int(format(i, f"0{bits}b")[::-1], 2) if bits else 0
+    return r
+
+
+# ---------------------------------------------------------------------------------------
+# baby-step / giant-step plan of one diagonal matrix
+# ---------------------------------------------------------------------------------------
+
+@dataclass
+class BsgsPlan:
+    unit: int                    # all offsets are multiples of `unit`
+    g: int                       # baby-step span
+    baby: list                   # baby rotation amounts (slots), 0 first
+    giants: dict                 # k -> {b: diag pre-rotated by -k*g*unit}
+    n: int
+
+    def rotations(self) -> set:
+        r = {b % self.n for b in self.baby if b % self.n}
+        r |= {(k * self.g * self.unit) % self.n for k in self.giants if (k * self.g * self.unit) % self.n}
+        return r
+
+
+def bsgs_plan(M: DiagMat, n: int) -> BsgsPlan:
+    offs = sorted(M)
+    signed = [d if d <= n // 2 else d - n for d in offs]
+    nz = [abs(s) for s in signed if s]
+    unit = 1
+    if nz:
+        from math import gcd
+        unit = 0
+        for s in nz:
+            unit = gcd(unit, s)
+    ms = [s // unit for s in signed]
+    span = max(ms) - min(ms) + 1
+    g = 1
+    while g * g < span:
+        g *= 2
+    giants = {}
+    babies = set()
+    for d, m in zip(offs, ms):
+        b = m % g
+        k = (m - b) // g
+        babies.add(b)
+        shift = k * g * unit
+        giants.setdefault(k, {})[b] = np.roll(M[d], shift)
+    baby = sorted(babies)
+    return BsgsPlan(unit=unit, g=g, baby=[b * unit for b in baby], giants=giants, n=n)
+
+
+def bsgs_apply_plain(plan: BsgsPlan, z: np.ndarray) -> np.ndarray:
+    """Plaintext model of the homomorphic BSGS evaluation (for tests)."""
+    out = np.zeros_like(z, dtype=np.complex128)
+    for k, terms in plan.giants.items():
+        inner = np.zeros_like(z, dtype=np.complex128)
+        for b in plan.baby:
+            if b // plan.unit in terms:
+                inner += terms[b // plan.unit] * np.roll(z, -b)
+        out += np.roll(inner, -k * plan.g * plan.unit)
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# EvalMod polynomial (Chebyshev basis)
+# ---------------------------------------------------------------------------------------
+
+def cheb_interp(f, deg: int) -> np.ndarray:
+    """Chebyshev coefficients of the degree-`deg` interpolant of f on [-1, 1]."""
+    from numpy.polynomial import chebyshev as C
+    k = np.arange(deg + 1)
+    x = np.cos(np.pi * (k + 0.5) / (deg + 1))
+    return C.chebfit(x, f(x), deg)
+
+
+def cheb_divmod(c: np.ndarray, G: int):
+    """p = q T_G + r in the Chebyshev basis (T_{G+j} = 2 T_G T_j - T_{G-j}); deg p < 2G."""
+    c = np.array(c, dtype=np.float64)
+    deg = len(c) - 1
+    q = np.zeros(max(deg - G + 1, 1))
+    r = np.array(c[:G], dtype=np.float64) if deg >= G else c.copy()
+    if deg < G:
+        return np.zeros(1), r
+    for j in range(deg - G, -1, -1):
+        a = c[G + j]
+        if j == 0:
+            q[0] += a
+        else:
+            q[j] += 2 * a
+            r[G - j] -= a
+    return q, r
+
+
+@dataclass(frozen=True)
+class BootConfig:
+    cts_levels: int = 4
+    stc_levels: int = 3
+    K: int = 16                  # |t/q0| <= K (I bound + margin for h = 64)
+    r: int = 3                   # double angles
+    cheb_degree: int = 31
+    baby: int = 8                # Chebyshev baby steps T_0..T_7
+
+
+def evalmod_constants(cfg: BootConfig):
+    """alpha, beta (u = alpha x + beta), Chebyshev coefficients of s0 cos(2 pi Y u), and the
+    double-angle offsets s_1..s_r with c_{k+1} = c_k^2 - s_{k+1} giving sin(2 pi x)/(2 pi)."""
+    Y = (cfg.K + 0.25) / 2 ** cfg.r
+    alpha = 1.0 / (cfg.K + 0.25)
+    beta = -0.25 / (cfg.K + 0.25)
+    s = [1.0 / (2 * pi)]
+    for _ in range(cfg.r):
+        s.append(float(np.sqrt(2 * s[-1])))
+    s = s[::-1]                  # s[0] = s0, s[r] = 1/(2 pi)
+    coeffs = cheb_interp(lambda u: s[0] * np.cos(2 * pi * Y * u), cfg.cheb_degree)
+    return alpha, beta, coeffs, s[1:]
+
+
+def evalmod_plain(x: np.ndarray, cfg: BootConfig) -> np.ndarray:
+    from numpy.polynomial import chebyshev as C
+    alpha, beta, coeffs, s = evalmod_constants(cfg)
+    c = C.chebval(alpha * x + beta, coeffs)
+    for sk in s:
+        c = c * c - sk
+    return c
+
+
+# ---------------------------------------------------------------------------------------
+# the algorithm over a backend
+# ---------------------------------------------------------------------------------------
+
+class Bootstrapper:
+    """Precomputes the plaintext diagonals of CoeffToSlot / SlotToCoeff for `params` and runs
+    the pipeline over `backend` (GpuBackend for the product)."""
+
+    def __init__(self, backend, cfg: BootConfig = BootConfig()):
+        self.be = backend
+        self.cfg = cfg
+        self.N = backend.N
+        self.n = self.N // 2
+        self.q = list(backend.main_primes)
+        self.L = len(self.q) - 1
+        self.q0 = self.q[0]
+        self.alpha, self.beta, self.cheb, self.dbl = evalmod_constants(cfg)
+        self.out_scale = Fraction(getattr(backend, "default_scale", 1 << 26))
+        self._build_linear()
+
+    # -- planning --------------------------------------------------------------------
+    def _build_linear(self):
+        cfg, n = self.cfg, self.n
+        cts = cts_matrices(self.N, cfg.cts_levels)
+        stc = stc_matrices(self.N, cfg.stc_levels)
+        # fold alpha * (q-relative) constants: CtS output y = alpha/2 * (t_k + i t_{k+n}) / q0
+        # given input slots z = Embed(t)/Delta_in; Delta_in varies, so the factor Delta_in/q0
+        # is applied through the declared scale (see bootstrap()).  Balance the magnitude over
+        # the levels so every diagonal is O(1) (plaintext precision).
+        self.cts_plans = [bsgs_plan(M, n) for M in cts]
+        self.stc_plans = [bsgs_plan(M, n) for M in stc]
+        self.cts_const = self.alpha / 2
+        self.rotations = set()
+        for pl in self.cts_plans + self.stc_plans:
+            self.rotations |= pl.rotations()
+        # level schedule
+        l = self.L
+        self.cts_at = []
+        for i in range(cfg.cts_levels):
+            self.cts_at.append(l)
+            l -= 2
+        self.evalmod_in = l
+        self._pt_cache = {}
+
+    def required_rotations(self) -> list:
+        return sorted(self.rotations)
+
+    def levels_used(self) -> dict:
+        return {"cts": self.cts_at, "evalmod_in": self.evalmod_in}
+
+    # -- helpers ---------------------------------------------------------------------
+    def _pt(self, key, vec, level, scale):
+        k = (key, level, scale)
+        pt = self._pt_cache.get(k)
+        if pt is None:
+            pt = self.be.encode_slots(vec, level, scale)
+            self._pt_cache[k] = pt
+        return pt
+
+    def _linear(self, ct, plan: BsgsPlan, tag, const, S_p, nres: int):
+        """sum_d diag_d * rot(ct, d) with BSGS: diagonals (times `const`) encoded at the
+        plaintext scale S_p, then `nres` rescales."""
+        be = self.be
+        l = ct.level
+        S_p = Fraction(S_p)
+        rots = be.rotate_hoisted(ct, plan.baby)
+        rmap = dict(zip(plan.baby, rots))
+        inners = []
+        for k in sorted(plan.giants):
+            terms = plan.giants[k]
+            pairs = []
+            for b in plan.baby:
+                bu = b // plan.unit
+                if bu in terms:
+                    pt = self._pt((tag, k, bu), terms[bu] * const, l, S_p)
+                    pairs.append((rmap[b], pt))
+            inners.append((k, be.mul_plain_sum(pairs)))
+        giant_steps = [(k * plan.g * plan.unit) % self.n for k, _ in inners]
+        acc = None
+        for c in be.rotate_many([c for _, c in inners], giant_steps):
+            acc = c if acc is None else be.add(acc, c)
+        for _ in range(nres):
+            acc = be.rescale(acc)
+        return acc
+
+    def _match(self, ct, level, scale):
+        """ct (level >= level+1) -> (level, scale) via multiplication by the constant 1
+        encoded at the exact compensating scale (two primes: precision ~2^-52)."""
+        be = self.be
+        assert ct.level >= level + 2, (ct.level, level)
+        ct = be.drop_to_level(ct, level + 2)
+        S_p = Fraction(scale) * self.q[level + 2] * self.q[level + 1] / Fraction(ct.scale)
+        out = be.mul_const(ct, 1.0, S_p)
+        out = be.rescale(be.rescale(out))
+        assert out.level == level and out.scale == scale
+        return out
+
+    def _mul2(self, a, b):
+        """a * b, relinearised, then two rescales (double-prime level)."""
+        be = self.be
+        lv = min(a.level, b.level)
+        a, b = be.drop_to_level(a, lv), be.drop_to_level(b, lv)
+        return be.rescale(be.rescale(be.hom_mul(a, b)))
+
+    def _cheb_powers(self, u):
+        be = self.be
+        T = {1: u}
+        g = self.cfg.baby
+
+        def double(k):                          # T_2k = 2 T_k^2 - 1
+            x = self._mul2(T[k], T[k])
+            x = be.add(x, x)
+            return be.add_const(x, -1.0)
+
+        def odd(k):                             # T_2k+1 = 2 T_k T_k+1 - T_1
+            x = self._mul2(T[k], T[k + 1])
+            x = be.add(x, x)
+            return be.sub(x, self._match(T[1], x.level, x.scale))
+
+        for m in range(2, g):
+            T[m] = double(m // 2) if m % 2 == 0 else odd(m // 2)
+        G = g
+        while G <= self.cfg.cheb_degree:
+            T[G] = double(G // 2)
+            G *= 2
+        return T
+
+    def _leaf(self, c, T, level, scale):
+        """sum_i c_i T_i (i < baby) at exactly (level, scale)."""
+        be = self.be
+        acc = None
+        for i in range(1, len(c)):
+            if c[i] == 0.0:
+                continue
+            t = T[i]
+            assert t.level >= level + 2, (i, t.level, level)
+            t = be.drop_to_level(t, level + 2)
+            S_p = Fraction(scale) * self.q[level + 2] * self.q[level + 1] / Fraction(t.scale)
+            term = be.rescale(be.rescale(be.mul_const(t, float(c[i]), S_p)))
+            acc = term if acc is None else be.add(acc, term)
+        assert acc is not None
+        return be.add_const(acc, float(c[0]))
+
+    def _feasible(self, c, T, t):
+        g = self.cfg.baby
+        if len(c) <= g:
+            need = min(T[i].level for i in range(1, len(c)) if c[i] != 0.0)
+            return t + 2 <= need
+        G = self._giant_for(len(c) - 1)
+        q, r = cheb_divmod(c, G)
+        return (t + 2 <= T[G].level and self._feasible(q, T, t + 2)
+                and self._feasible(r, T, t))
+
+    def _giant_for(self, deg):
+        G = self.cfg.baby
+        while 2 * G <= deg:
+            G *= 2
+        return G
+
+    def _cheb_eval(self, c, T, level, scale):
+        be = self.be
+        g = self.cfg.baby
+        c = np.trim_zeros(np.asarray(c, dtype=np.float64), "b")
+        if len(c) <= g:
+            return self._leaf(c, T, level, scale)
+        G = self._giant_for(len(c) - 1)
+        q, r = cheb_divmod(c, G)
+        m = level + 2
+        TG = be.drop_to_level(T[G], m)
+        q_scale = Fraction(scale) * self.q[m] * self.q[m - 1] / Fraction(TG.scale)
+        qc = self._cheb_eval(q, T, m, q_scale)
+        prod = be.rescale(be.rescale(be.hom_mul(qc, TG)))
+        assert prod.level == level and prod.scale == scale
+        rc = self._cheb_eval(r, T, level, scale)
+        return be.add(prod, rc)
+
+    def _evalmod(self, x):
+        """x: slots in [-K, K] (already u = alpha x + beta) -> sin(2 pi x)/(2 pi)."""
+        be = self.be
+        T = self._cheb_powers(x)
+        c = self.cheb
+        t = T[1].level - 2
+        while t >= 0 and not self._feasible(c, T, t):
+            t -= 1
+        if t < 0:
+            raise ValueError("not enough levels for EvalMod")
+        scale = Fraction(self.q[t + 1]) * self.q[t + 2]
+        y = self._cheb_eval(c, T, t, scale)
+        for sk in self.dbl:
+            y = self._mul2(y, y)
+            y = be.add_const(y, -sk)
+        return y
+
+    # -- the pipeline ----------------------------------------------------------------
+    def bootstrap(self, ct, out_scale=None):
+        """Refresh a level-0 ciphertext; returns a ciphertext at level
+        L - (2 cts_levels - 1) - 2 (EvalMod depth) - (stc_levels + 1) with scale `out_scale`
+        (default: the parameter set's scale)."""
+        be = self.be
+        if ct.level != 0:
+            ct = be.drop_to_level(ct, 0)
+        delta_in = Fraction(ct.scale)
+        q = self.q
+        x = be.mod_raise(ct)                                  # level L, scale Delta_in
+        # Lift the integers to a ~2^52 scale with an exact integer multiplication (no level):
+        # the keyswitch and rescale noise of CoeffToSlot is absolute, the slots are dominated
+        # by q0*I, and m/q0 must survive at ~2^-40 relative precision.
+        lift = 1 << max(0, 52 - int(delta_in).bit_length())
+        if lift > 1:
+            x = be.mul_const(x, 1.0, lift)
+        # CoeffToSlot: plaintext diagonals at q_l q_{l-1} (~2^52) and two rescales per level;
+        # the last level folds alpha/2 * Delta_in/q0 and lands exactly on the EvalMod working
+        # scale q_l' q_{l'-1} (l' = its output level).
+        c0 = self.cts_const * float(delta_in) / self.q0
+        nc = len(self.cts_plans)
+        for i, plan in enumerate(self.cts_plans):
+            l = x.level
+            if i < nc - 1:
+                x = self._linear(x, plan, ("cts", i), 1.0, Fraction(q[l]) * q[l - 1], 2)
+            else:
+                lo = l - 2
+                S_p = Fraction(q[lo]) * q[lo - 1] * q[l] * q[l - 1] / Fraction(x.scale)
+                x = self._linear(x, plan, ("cts", i, float(delta_in)), c0, S_p, 2)
+        # conjugation split (both EvalMod inputs carry the same level and scale)
+        xc = be.conjugate(x)
+        re = be.add(x, xc)
+        im = be.mul_monomial(be.sub(x, xc), 3 * self.N // 2)   # * (-i) = * X^(3N/2)
+        re = be.add_const(re, self.beta)
+        im = be.add_const(im, self.beta)
+        re = self._evalmod(re)
+        im = self._evalmod(im)
+        y = be.add(re, be.mul_monomial(im, self.N // 2))       # re + i im
+        # SlotToCoeff: the first level folds q0/Delta_in, the last lands on out_scale
+        out_scale = Fraction(self.out_scale if out_scale is None else out_scale)
+        c1 = self.q0 / float(delta_in)
+        ns = len(self.stc_plans)
+        for i, plan in enumerate(self.stc_plans):
+            l = y.level
+            const = c1 if i == 0 else 1.0
+            tag = ("stc", i, float(delta_in)) if i == 0 else ("stc", i)
+            if i < ns - 1:
+                y = self._linear(y, plan, tag, const, Fraction(q[l]), 1)
+            else:
+                S_p = out_scale * q[l] * q[l - 1] / Fraction(y.scale)
+                y = self._linear(y, plan, tag, const, S_p, 2)
+        return y
+
+
+# ---------------------------------------------------------------------------------------
+# GPU backend (the product): every operation is a kernel of libcerium_b200.so
+# ---------------------------------------------------------------------------------------
+
+def encode_ints(values, N: int, scale) -> np.ndarray:
+    """Integer coefficients round(embed_inverse(values) * scale) of a (complex) slot vector,
+    the reference's encode arithmetic (encoding.py:82-105) without the range check."""
+    r = np.rint(embed_inverse(np.asarray(values, dtype=np.complex128), N) * float(scale))
+    if np.abs(r).max(initial=0.0) >= 2.0 ** 62:
+        raise OverflowError("plaintext coefficients exceed int64")
+    return r.astype(np.int64)
+
+
+def monomial_ints(N: int, e: int) -> np.ndarray:
+    """Coefficients of X^e in Z[X]/(X^N + 1)."""
+    c = np.zeros(N, dtype=np.int64)
+    e %= 2 * N
+    c[e % N] = -1 if e >= N else 1
+    return c
+
+
+class GpuBackend:
+    """Bootstrap backend over the B200 operator API (ckks.py / fused.py kernels)."""
+
+    def __init__(self, params, relin_key, conj_key, rot_keys: dict):
+        from . import ckks as C
+        self.C = C
+        self.params = params
+        self.N = params.N
+        self.main_primes = tuple(params.rns_basis)
+        self.default_scale = params.scale
+        self.rlk = relin_key
+        self.ck = conj_key
+        self.rk = rot_keys
+        self._mono = {}
+
+    # ciphertext plumbing
+    def drop_to_level(self, ct, level):
+        C = self.C
+        if ct.level == level:
+            return ct
+        assert level < ct.level
+        from .poly import RnsPolynomial, main_ids
+        ids = main_ids(level)
+        return C.Ciphertext(RnsPolynomial(ct.b.limbs[: level + 1], ct.b.domain, ids),
+                            RnsPolynomial(ct.a.limbs[: level + 1], ct.a.domain, ids),
+                            ct.scale, level)
+
+    def mod_raise(self, ct):
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .poly import Domain, RnsPolynomial, main_ids, ntt_rows
+        p = self.params
+        L = p.max_level
+        rows = torch.stack([ct.b.limbs[0], ct.a.limbs[0]])
+        ntt_rows(p, rows, (0, 0), inverse=True)
+        out = torch.empty((2, L + 1, p.N), dtype=torch.int32, device=rows.device)
+        ctx = get_context(p)
+        _native.check(_native.lib().lf_modraise(ctx.handle, dptr(out), dptr(rows), 2, L + 1,
+                                                stream_handle()), "lf_modraise")
+        ids = main_ids(L)
+        ntt_rows(p, out.view(2 * (L + 1), p.N), ids + ids)
+        return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale, L)
+
+    def encode_slots(self, values, level, scale):
+        from .encoding import Plaintext, signed_to_eval
+        from .poly import main_ids
+        ints = encode_ints(values, self.params.N, scale)
+        return Plaintext(signed_to_eval(ints, self.params, main_ids(level)), Fraction(scale), level)
+
+    # arithmetic
+    def add(self, x, y):
+        return self.C.hom_add(x, y, self.params)
+
+    def sub(self, x, y):
+        return self.C.hom_sub(x, y, self.params)
+
+    def rescale(self, x):
+        return self.C.rescale(x, self.params)
+
+    def hom_mul(self, x, y):
+        return self.C.hom_mul(x, y, self.rlk, self.params)
+
+    def conjugate(self, x):
+        return self.C.hom_conjugate(x, self.ck, self.params)
+
+    def rotate_hoisted(self, x, steps):
+        return self.C.hom_rotate_hoisted(x, list(steps), self.rk, self.params)
+
+    def rotate_many(self, xs, steps):
+        return [x if s % self.params.n == 0 else
+                self.C.hom_rotate(x, s, self.rk[s % self.params.n], self.params)
+                for x, s in zip(xs, steps)]
+
+    def mul_plain_sum(self, pairs):
+        import torch
+        from . import _native
+        from .context import get_context, stream_handle
+        from .poly import Domain, RnsPolynomial, main_ids
+        ct0, pt0 = pairs[0]
+        level = ct0.level
+        N = self.params.N
+        out = torch.empty((2, level + 1, N), dtype=torch.int32, device=ct0.b.limbs.device)
+        ctx = get_context(self.params)
+        lib = _native.lib()
+        for i in range(0, len(pairs), 32):
+            chunk = pairs[i: i + 32]
+            n = len(chunk)
+            bp = (ctypes_void_p * n)(*[c.b.limbs.data_ptr() for c, _ in chunk])
+            ap = (ctypes_void_p * n)(*[c.a.limbs.data_ptr() for c, _ in chunk])
+            pp = (ctypes_void_p * n)(*[pt.poly.limbs.data_ptr() for _, pt in chunk])
+            assert all(c.level == level and pt.level == level for c, pt in chunk)
+            tgt = out if i == 0 else torch.empty_like(out)
+            _native.check(lib.lf_ptmac(ctx.handle, ctypes_void_p(tgt.data_ptr()), level + 1, n,
+                                       bp, ap, pp, stream_handle()), "lf_ptmac")
+            if i:
+                out = torch.stack([self._addrows(out[0], tgt[0], level), self._addrows(out[1], tgt[1], level)])
+        ids = main_ids(level)
+        scale = ct0.scale * pt0.scale
+        return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[1], Domain.EVAL, ids), scale, level)
+
+    def _addrows(self, x, y, level):
+        from .poly import LF_OP_ADD, ewise, main_ids
+        o = x.clone()
+        ewise(self.params, LF_OP_ADD, o, x, main_ids(level), b=y)
+        return o
+
+    def _scalar_rows(self, ct, k: int):
+        return [k % q for q in self.params.rns_basis[: ct.level + 1]]
+
+    def mul_const(self, ct, c: float, S_p):
+        """ct * round(c * S_p) with the declared plaintext scale S_p (no rescale)."""
+        import torch
+        from .poly import LF_OP_SCALAR_MUL, Domain, RnsPolynomial, ewise, main_ids
+        k = round(Fraction(c) * Fraction(S_p))
+        ids = main_ids(ct.level)
+        sc = self._scalar_rows(ct, k)
+        out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
+        ewise(self.params, LF_OP_SCALAR_MUL, out[0], ct.b.limbs, ids, scalars=sc)
+        ewise(self.params, LF_OP_SCALAR_MUL, out[1], ct.a.limbs, ids, scalars=sc)
+        return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale * Fraction(S_p), ct.level)
+
+    def add_const(self, ct, c: float):
+        """ct + c (the constant encoded at the ciphertext's own scale; b only)."""
+        import torch
+        from .poly import LF_OP_ADD_SCALAR, Domain, RnsPolynomial, ewise, main_ids
+        k = round(Fraction(c) * Fraction(ct.scale))
+        ids = main_ids(ct.level)
+        out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
+        ewise(self.params, LF_OP_ADD_SCALAR, out[0], ct.b.limbs, ids, scalars=self._scalar_rows(ct, k))
+        out[1].copy_(ct.a.limbs)
+        return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale, ct.level)
+
+    def mul_monomial(self, ct, e: int):
+        """ct * X^e (exact: slots times zeta^(e 5^j); X^(N/2) multiplies every slot by i)."""
+        from .encoding import Plaintext, signed_to_eval
+        from .poly import main_ids
+        key = (e, ct.level)
+        pt = self._mono.get(key)
+        if pt is None:
+            pt = Plaintext(signed_to_eval(monomial_ints(self.params.N, e), self.params,
+                                          main_ids(ct.level)), Fraction(1), ct.level)
+            self._mono[key] = pt
+        return self.C.mul_plain(ct, pt, self.params)
+
+
+from ctypes import c_void_p as ctypes_void_p  # noqa: E402
+
+
+def make_bootstrap_keys(params, sk, rotations, seed: int = 99):
+    """Conjugation key and the rotation keys a Bootstrapper needs (host RNG in the reference's
+    draw order per key, keys.py:129-159)."""
+    from .keys import make_conjugation_key, make_rotation_key
+    rng = np.random.default_rng(seed)
+    ck = make_conjugation_key(params, sk, rng)
+    rk = {}
+    for s in sorted(rotations):
+        rk[s] = make_rotation_key(params, sk, s, rng)
+    return ck, rk

@@ -149,7 +149,7 @@ int lf_ewise(const lf_ctx* ctx, int op, uint32_t* out, const uint32_t* a, const 
              const uint32_t* c, int nrows, const int32_t* pidx, const uint32_t* scalars,
              void* stream) {
   if (!ctx || !out || !a || (!pidx && nrows)) { lf_set_error("lf_ewise: null argument"); return 1; }
-  if (op < LF_OP_ADD || op > LF_OP_MUL_SCALAR_ADD) { lf_set_error("lf_ewise: bad op %d", op); return 2; }
+  if (op < LF_OP_ADD || op > LF_OP_ADD_SCALAR) { lf_set_error("lf_ewise: bad op %d", op); return 2; }
   const bool needs_b = op == LF_OP_ADD || op == LF_OP_SUB || op == LF_OP_MUL || op == LF_OP_MULACC ||
                        op == LF_OP_MODSTEP || op == LF_OP_MUL_SCALAR_ADD;
   if (needs_b && !b) { lf_set_error("lf_ewise: op %d needs b", op); return 1; }
@@ -180,6 +180,23 @@ int lf_bconv(const lf_ctx* ctx, uint32_t* out, const uint32_t* src, const uint32
              int k, int m, int W, void* stream) {
   if (!ctx || !out || !src || !table) { lf_set_error("lf_bconv: null argument"); return 1; }
   return lf_launch_bconv(ctx, out, src, table, k, m, W, (cudaStream_t)stream);
+}
+
+int lf_modraise(const lf_ctx* ctx, uint32_t* out, const uint32_t* in, int nin, int nout,
+                void* stream) {
+  if (!ctx || !out || !in) { lf_set_error("lf_modraise: null argument"); return 1; }
+  if (nout < 1 || nout > ctx->nprimes || nin < 1) { lf_set_error("lf_modraise: bad row counts"); return 2; }
+  return lf_launch_modraise(ctx, out, in, nin, nout, (cudaStream_t)stream);
+}
+
+int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+             const uint32_t* const* a, const uint32_t* const* pt, void* stream) {
+  if (!ctx || !out || !b || !a || !pt) { lf_set_error("lf_ptmac: null argument"); return 1; }
+  if (nterm < 1 || nterm > LF_PTMAC_MAX) { lf_set_error("lf_ptmac: nterm %d outside [1, %d]", nterm, LF_PTMAC_MAX); return 2; }
+  if (nrows < 1 || nrows > ctx->nprimes) { lf_set_error("lf_ptmac: bad nrows %d", nrows); return 2; }
+  for (int i = 0; i < nterm; ++i)
+    if (!b[i] || !a[i] || !pt[i]) { lf_set_error("lf_ptmac: null term %d", i); return 1; }
+  return lf_launch_ptmac(ctx, out, nrows, nterm, b, a, pt, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -27,6 +27,7 @@ LF_DEV u32 ew_one(int op, u32 a, u32 b, u32 c, u32 s, u32 sp, const PrimeK& k) {
     case LF_OP_MULACC: return reduce64((u64)a * b + c, k);
     case LF_OP_MODSTEP: return mul_shoup(submod(a, b, q), s, sp, q);
     case LF_OP_MUL_SCALAR_ADD: return addmod(mul_shoup(a, s, sp, q), b, q);   // a*s + b
+    case LF_OP_ADD_SCALAR: return addmod(a, s, q);                              // a + s
     default: return 0u;
   }
 }
@@ -86,6 +87,87 @@ __global__ void __launch_bounds__(128) k_bconv(u32* out, const u32* src, BconvDe
     for (int i = 0; i < B.k; ++i) acc += (u64)y[i] * B.w[(size_t)t * B.k + i];
     out[t * N + n] = reduce64(acc, kt);
   }
+}
+
+// ModRaise (bootstrap): coefficient rows mod q0 -> centred lift in (-q0/2, q0/2] reduced into
+// the primes of nout rows: out[i*nout + r] = lift(in[i]) mod q_r.
+__global__ void __launch_bounds__(256) k_modraise(u32* out, const u32* in, int nin, int nout,
+                                                  LfDev dv) {
+  const size_t N = (size_t)1 << dv.logN;
+  const u32 q0 = dv.pk[0].q;
+  const size_t total = N * nin * nout;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t pos = idx & (N - 1);
+    const size_t rr = idx >> dv.logN;            // i * nout + r
+    const int r = (int)(rr % nout), i = (int)(rr / nout);
+    const PrimeK k = dv.pk[r];
+    const u32 c = in[(size_t)i * N + pos];
+    u32 v;
+    if (c > q0 / 2) {
+      const u32 m = reduce32(q0 - c, k);        // (c - q0) mod q_r = -( (q0 - c) mod q_r )
+      v = m ? k.q - m : 0u;
+    } else {
+      v = reduce32(c, k);
+    }
+    out[idx] = v;
+  }
+}
+
+// Plaintext multiply-accumulate over terms (bootstrap linear transforms):
+// out[p][r] = sum_i ct_i[p][r] * pt_i[r]  (p in {b, a}, r < nrows), 64-bit lazy sums.
+struct PtMacArgs {
+  u32* out;                 // 2 x nrows rows
+  int nterm, nrows;
+  const u32* b[LF_PTMAC_MAX];
+  const u32* a[LF_PTMAC_MAX];
+  const u32* pt[LF_PTMAC_MAX];
+};
+
+__global__ void __launch_bounds__(256) k_ptmac(PtMacArgs A, LfDev dv) {
+  const int row = blockIdx.y;                   // 0 .. 2*nrows-1
+  const int p = row / A.nrows, r = row % A.nrows;
+  const PrimeK k = dv.pk[r];
+  const size_t N = (size_t)1 << dv.logN;
+  const size_t off = (size_t)r * N;
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < N / 4;
+       v += (size_t)gridDim.x * blockDim.x) {
+    u64 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    for (int i = 0; i < A.nterm; ++i) {
+      const u32* src = p ? A.a[i] : A.b[i];
+      const uint4 x = reinterpret_cast<const uint4*>(src + off)[v];
+      const uint4 y = reinterpret_cast<const uint4*>(A.pt[i] + off)[v];
+      acc0 += (u64)x.x * y.x;
+      acc1 += (u64)x.y * y.y;
+      acc2 += (u64)x.z * y.z;
+      acc3 += (u64)x.w * y.w;
+    }
+    reinterpret_cast<uint4*>(A.out + (size_t)row * N)[v] =
+        make_uint4(reduce64(acc0, k), reduce64(acc1, k), reduce64(acc2, k), reduce64(acc3, k));
+  }
+}
+
+int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
+                       cudaStream_t s) {
+  const size_t total = (size_t)ctx->N * nin * nout;
+  size_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_modraise<<<(unsigned)blocks, 256, 0, s>>>(out, in, nin, nout, ctx->dev());
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
+int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
+                    const u32* const* a, const u32* const* pt, cudaStream_t s) {
+  PtMacArgs A;
+  A.out = out; A.nterm = nterm; A.nrows = nrows;
+  for (int i = 0; i < nterm; ++i) { A.b[i] = b[i]; A.a[i] = a[i]; A.pt[i] = pt[i]; }
+  const int nv = ctx->N / 4;
+  const int bx = (nv + 255) / 256 < 16 ? (nv + 255) / 256 : 16;
+  dim3 grid(bx, 2 * nrows);
+  k_ptmac<<<grid, 256, 0, s>>>(A, ctx->dev());
+  LF_CHECK_LAUNCH();
+  return 0;
 }
 
 int lf_launch_ewise(const LfCtx* ctx, int op, u32* out, const u32* a, const u32* b,

@@ -9,3 +9,9 @@ int lf_launch_automorph(const LfCtx* ctx, u32* out, const u32* in, u32 g, int nr
                         cudaStream_t s);
 int lf_launch_bconv(const LfCtx* ctx, u32* out, const u32* src, const u32* tab, int k, int m,
                     int W, cudaStream_t s);
+
+#define LF_PTMAC_MAX 32
+int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
+                       cudaStream_t s);
+int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
+                    const u32* const* a, const u32* const* pt, cudaStream_t s);

@@ -17,6 +17,7 @@ from .params import CkksParams
 
 LF_OP_ADD, LF_OP_SUB, LF_OP_MUL, LF_OP_NEG = 0, 1, 2, 3
 LF_OP_SCALAR_MUL, LF_OP_MULACC, LF_OP_MODSTEP, LF_OP_MUL_SCALAR_ADD = 4, 5, 6, 7
+LF_OP_ADD_SCALAR = 8
 
 
 class Domain(Enum):

@@ -1,0 +1,45 @@
+"""Time the N=2^16 bootstrap (C3 variant) on cuda:0: setup, eager latency, precision."""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_11269_b200 as B  # noqa: E402
+from paper_2512_11269_b200 import bootstrap as BT  # noqa: E402
+
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 47
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+t0 = time.time()
+p = B.gen_params(65536, L, d=4, seed=0, scale=2 ** 26)
+sk, pk, rlk = B.keygen(p, seed=11)
+cfg = BT.BootConfig()
+planner = BT.Bootstrapper(type("P", (), {"N": p.N, "main_primes": p.rns_basis}), cfg)
+rots = planner.required_rotations()
+ck, rk = BT.make_bootstrap_keys(p, sk, rots, seed=99)
+torch.cuda.synchronize()
+print(f"keys: {len(rots)} rotations + conj, {time.time() - t0:.1f} s", flush=True)
+v = np.random.default_rng(77).uniform(-1, 1, p.n)
+ct = B.encrypt(B.encode(v, p, level=0, scale=2 ** 26), pk, p, np.random.default_rng(5))
+bt = BT.Bootstrapper(BT.GpuBackend(p, rlk, ck, rk), cfg)
+t0 = time.time()
+out = bt.bootstrap(ct)
+torch.cuda.synchronize()
+print(f"first bootstrap (plaintext encoding included): {time.time() - t0:.2f} s; out level {out.level}", flush=True)
+din = B.decrypt(ct, sk, p)
+dout = B.decrypt(out, sk, p)
+e1, e2 = np.abs(dout - din).max(), np.abs(dout - v).max()
+print(f"precision: vs input decryption {e1:.3e} ({-np.log2(e1):.1f} bits), vs plaintext {e2:.3e} ({-np.log2(e2):.1f} bits)")
+ms = []
+for _ in range(reps):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record()
+    out = bt.bootstrap(ct)
+    b.record()
+    torch.cuda.synchronize()
+    ms.append((a.elapsed_time(b), (time.perf_counter() - w0) * 1e3))
+print("eager bootstrap ms (device, wall):", [(round(x, 2), round(y, 2)) for x, y in ms])
