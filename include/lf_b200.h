@@ -137,6 +137,13 @@ size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,
                uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
 
+/* rescale by the top ndrop in {1, 2} primes: ndrop = 2 equals two successive lf_rescale calls
+ * (ckks.py:220-225 twice) bit for bit, in one pass.  out = 2 x (level + 1 - ndrop) rows;
+ * workspace as lf_rescale. */
+int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct,
+                     size_t ct_bstride, uint32_t* out, size_t out_bstride, int batch,
+                     void* workspace, void* stream);
+
 /* keyswitch_decompose (ckks.py:95-117) materialised: pieces = beta x (level+1+alpha) rows,
  * eval domain, digit-major; beta = min(d, level+1).  Workspace as lf_keyswitch (batch 1). */
 int lf_ks_decompose(const lf_ctx* ctx, int level, const uint32_t* x, uint32_t* pieces,
@@ -156,6 +163,12 @@ int lf_modraise(const lf_ctx* ctx, uint32_t* out, const uint32_t* in, int nin, i
  * (ckks.py:152-179) term by term. */
 int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
              const uint32_t* const* a, const uint32_t* const* pt, void* stream);
+
+/* Linear combination with constants: out (2 x nrows rows) = sum_i k_i * (b_i, a_i) over
+ * nterm <= 8 terms; k is a HOST array [nterm][nrows] of per-row constants (any uint32, reduced
+ * mod the row's prime).  Equals poly_scalar_mul + poly_add (poly.py:183-209) term by term. */
+int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+               const uint32_t* const* a, const uint32_t* k, void* stream);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,16 @@ class OracleBackend:
     def rescale(self, x):
         return O.rescale(self.P, x)
 
+    def rescale2(self, x):
+        return O.rescale(self.P, O.rescale(self.P, x))
+
+    def lincomb(self, terms):
+        acc = None
+        for ct, c, S in terms:
+            t = self.mul_const(ct, c, S)
+            acc = t if acc is None else O.hom_add(self.P, acc, t)
+        return acc
+
     def hom_mul(self, x, y):
         return O.hom_mul(self.P, x, y, self.rlk)
 

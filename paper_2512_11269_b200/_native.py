@@ -59,6 +59,11 @@ def _load():
         "lf_rescale_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                       ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_rescale_multi": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, ctypes.c_size_t,
+                                            _u32p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_lincomb": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                      _u32_host, ctypes.c_void_p]),
         "lf_ks_decompose": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, _u32p, ctypes.c_void_p,
                                            ctypes.c_void_p]),
         "lf_modraise": (ctypes.c_int, [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_int,

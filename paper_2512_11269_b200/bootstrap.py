@@ -374,9 +374,7 @@ class Bootstrapper:
         acc = None
         for c in be.rotate_many([c for _, c in inners], giant_steps):
             acc = c if acc is None else be.add(acc, c)
-        for _ in range(nres):
-            acc = be.rescale(acc)
-        return acc
+        return be.rescale2(acc) if nres == 2 else be.rescale(acc)
 
     def _match(self, ct, level, scale):
         """ct (level >= level+1) -> (level, scale) via multiplication by the constant 1
@@ -385,8 +383,7 @@ class Bootstrapper:
         assert ct.level >= level + 2, (ct.level, level)
         ct = be.drop_to_level(ct, level + 2)
         S_p = Fraction(scale) * self.q[level + 2] * self.q[level + 1] / Fraction(ct.scale)
-        out = be.mul_const(ct, 1.0, S_p)
-        out = be.rescale(be.rescale(out))
+        out = be.rescale2(be.mul_const(ct, 1.0, S_p))
         assert out.level == level and out.scale == scale
         return out
 
@@ -395,7 +392,7 @@ class Bootstrapper:
         be = self.be
         lv = min(a.level, b.level)
         a, b = be.drop_to_level(a, lv), be.drop_to_level(b, lv)
-        return be.rescale(be.rescale(be.hom_mul(a, b)))
+        return be.rescale2(be.hom_mul(a, b))
 
     def _cheb_powers(self, u):
         be = self.be
@@ -421,9 +418,11 @@ class Bootstrapper:
         return T
 
     def _leaf(self, c, T, level, scale):
-        """sum_i c_i T_i (i < baby) at exactly (level, scale)."""
+        """sum_i c_i T_i (i < baby) at exactly (level, scale): every term is dropped to
+        level + 2 and multiplied by c_i encoded at the scale that makes all products share
+        scale * q_{level+2} q_{level+1}; one linear combination, one double rescale."""
         be = self.be
-        acc = None
+        terms = []
         for i in range(1, len(c)):
             if c[i] == 0.0:
                 continue
@@ -431,9 +430,10 @@ class Bootstrapper:
             assert t.level >= level + 2, (i, t.level, level)
             t = be.drop_to_level(t, level + 2)
             S_p = Fraction(scale) * self.q[level + 2] * self.q[level + 1] / Fraction(t.scale)
-            term = be.rescale(be.rescale(be.mul_const(t, float(c[i]), S_p)))
-            acc = term if acc is None else be.add(acc, term)
-        assert acc is not None
+            terms.append((t, float(c[i]), S_p))
+        assert terms
+        acc = be.rescale2(be.lincomb(terms))
+        assert acc.level == level and acc.scale == scale
         return be.add_const(acc, float(c[0]))
 
     def _feasible(self, c, T, t):
@@ -464,7 +464,7 @@ class Bootstrapper:
         TG = be.drop_to_level(T[G], m)
         q_scale = Fraction(scale) * self.q[m] * self.q[m - 1] / Fraction(TG.scale)
         qc = self._cheb_eval(q, T, m, q_scale)
-        prod = be.rescale(be.rescale(be.hom_mul(qc, TG)))
+        prod = be.rescale2(be.hom_mul(qc, TG))
         assert prod.level == level and prod.scale == scale
         rc = self._cheb_eval(r, T, level, scale)
         return be.add(prod, rc)
@@ -623,11 +623,53 @@ class GpuBackend:
     def rescale(self, x):
         return self.C.rescale(x, self.params)
 
+    def rescale2(self, x):
+        """Two successive rescales (ckks.py:220-225) fused into one pass (lf_rescale_multi)."""
+        from . import fused
+        if x.level < 2:
+            raise ValueError("double rescale below level 2")
+        b, a = fused.rescale_multi(self.params, x, 2)
+        q = self.params.rns_basis
+        return self.C.Ciphertext(b, a, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
+
     def hom_mul(self, x, y):
         return self.C.hom_mul(x, y, self.rlk, self.params)
 
     def conjugate(self, x):
         return self.C.hom_conjugate(x, self.ck, self.params)
+
+    def lincomb(self, terms):
+        """sum_i round(c_i S_i) * ct_i, all ct_i at one level with equal ct_i.scale * S_i."""
+        import torch
+        from . import _native
+        from .context import get_context, stream_handle
+        from .poly import Domain, RnsPolynomial, main_ids
+        ct0 = terms[0][0]
+        level = ct0.level
+        scale = Fraction(ct0.scale) * Fraction(terms[0][2])
+        nrows = level + 1
+        qs = self.params.rns_basis[:nrows]
+        out = None
+        ctx = get_context(self.params)
+        for i0 in range(0, len(terms), 8):
+            chunk = terms[i0: i0 + 8]
+            n = len(chunk)
+            ks = []
+            for ct, c, S in chunk:
+                assert ct.level == level and Fraction(ct.scale) * Fraction(S) == scale
+                k = round(Fraction(c) * Fraction(S))
+                ks.extend(k % q for q in qs)
+            tgt = torch.empty((2, nrows, self.params.N), dtype=torch.int32, device=ct0.b.limbs.device)
+            bp = (ctypes_void_p * n)(*[ct.b.limbs.data_ptr() for ct, _, _ in chunk])
+            ap = (ctypes_void_p * n)(*[ct.a.limbs.data_ptr() for ct, _, _ in chunk])
+            from . import _native as nat
+            _native.check(nat.lib().lf_lincomb(ctx.handle, ctypes_void_p(tgt.data_ptr()), nrows, n, bp, ap,
+                                               nat.u32_array(ks), stream_handle()), "lf_lincomb")
+            out = tgt if out is None else torch.stack([self._addrows(out[0], tgt[0], level),
+                                                        self._addrows(out[1], tgt[1], level)])
+        ids = main_ids(level)
+        return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[1], Domain.EVAL, ids), scale, level)
 
     def rotate_hoisted(self, x, steps):
         return self.C.hom_rotate_hoisted(x, list(steps), self.rk, self.params)

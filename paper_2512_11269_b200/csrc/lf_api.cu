@@ -199,4 +199,14 @@ int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint3
   return lf_launch_ptmac(ctx, out, nrows, nterm, b, a, pt, (cudaStream_t)stream);
 }
 
+int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+               const uint32_t* const* a, const uint32_t* k, void* stream) {
+  if (!ctx || !out || !b || !a || !k) { lf_set_error("lf_lincomb: null argument"); return 1; }
+  if (nterm < 1 || nterm > LF_LINCOMB_MAX) { lf_set_error("lf_lincomb: nterm %d outside [1, %d]", nterm, LF_LINCOMB_MAX); return 2; }
+  if (nrows < 1 || nrows > ctx->nprimes || nrows > LF_LINCOMB_ROWS) { lf_set_error("lf_lincomb: bad nrows %d", nrows); return 2; }
+  for (int i = 0; i < nterm; ++i)
+    if (!b[i] || !a[i]) { lf_set_error("lf_lincomb: null term %d", i); return 1; }
+  return lf_launch_lincomb(ctx, out, nrows, nterm, b, a, k, (cudaStream_t)stream);
+}
+
 }  // extern "C"

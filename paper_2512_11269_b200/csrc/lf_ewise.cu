@@ -147,6 +147,55 @@ __global__ void __launch_bounds__(256) k_ptmac(PtMacArgs A, LfDev dv) {
   }
 }
 
+// Linear combination with per-term, per-row constants (bootstrap polynomial leaves):
+// out[p][r] = sum_i k_i[r] * ct_i[p][r]  (p in {b, a}), 64-bit lazy sums.
+struct LinCombArgs {
+  u32* out;
+  int nterm, nrows;
+  const u32* b[LF_LINCOMB_MAX];
+  const u32* a[LF_LINCOMB_MAX];
+  u32 k[LF_LINCOMB_MAX][LF_LINCOMB_ROWS];
+};
+
+__global__ void __launch_bounds__(256) k_lincomb(LinCombArgs A, LfDev dv) {
+  const int row = blockIdx.y;
+  const int p = row / A.nrows, r = row % A.nrows;
+  const PrimeK k = dv.pk[r];
+  const size_t N = (size_t)1 << dv.logN;
+  const size_t off = (size_t)r * N;
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < N / 4;
+       v += (size_t)gridDim.x * blockDim.x) {
+    u64 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    for (int i = 0; i < A.nterm; ++i) {
+      const u32* src = p ? A.a[i] : A.b[i];
+      const uint4 x = reinterpret_cast<const uint4*>(src + off)[v];
+      const u32 c = A.k[i][r];
+      acc0 += (u64)x.x * c;
+      acc1 += (u64)x.y * c;
+      acc2 += (u64)x.z * c;
+      acc3 += (u64)x.w * c;
+    }
+    reinterpret_cast<uint4*>(A.out + (size_t)row * N)[v] =
+        make_uint4(reduce64(acc0, k), reduce64(acc1, k), reduce64(acc2, k), reduce64(acc3, k));
+  }
+}
+
+int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
+                      const u32* const* a, const u32* k, cudaStream_t s) {
+  LinCombArgs A;
+  A.out = out; A.nterm = nterm; A.nrows = nrows;
+  for (int i = 0; i < nterm; ++i) {
+    A.b[i] = b[i]; A.a[i] = a[i];
+    for (int r = 0; r < nrows; ++r) A.k[i][r] = k[(size_t)i * nrows + r] % ctx->h_pk[r].q;
+  }
+  const int nv = ctx->N / 4;
+  const int bx = (nv + 255) / 256 < 16 ? (nv + 255) / 256 : 16;
+  dim3 grid(bx, 2 * nrows);
+  k_lincomb<<<grid, 256, 0, s>>>(A, ctx->dev());
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
 int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
                        cudaStream_t s) {
   const size_t total = (size_t)ctx->N * nin * nout;

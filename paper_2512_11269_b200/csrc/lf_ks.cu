@@ -43,19 +43,20 @@ struct BcArgs {
 template <int L1, int L2, int MODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
-           size_t x_bs, size_t t_bs, int nrows, LfDev dv, int src_rs, int src_r0, int pfix) {
+           size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int GROUPS = (1 << L1) / S::LPCR;
   extern __shared__ __align__(16) u32 sm[];
   const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
   const int row = blockIdx.x / GROUPS, hi0 = (blockIdx.x % GROUPS) * S::LPCR, hi = hi0 + ln;
-  const int pi = pfix >= 0 ? pfix : row;
+  // row r: source row (r / rpp) * src_rs + src_r0 + r % rpp, prime pbase + r % rpp
+  const int pi = pbase + row % rpp;
   const PrimeK pk = dv.pk[pi];
   uint2* tws = reinterpret_cast<uint2*>(sm);
   stage_tree_async<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR,
                        threadIdx.x, blockDim.x);
-  const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)(row * src_rs + src_r0) << (L1 + L2)) +
+  const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) +
                      ((size_t)hi << L2);
   u32 v[C::E];
   load_row_step2<L2>(v, x + off, tl);
@@ -627,7 +628,7 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
 // Column tile width and group count: CW = 8 columns (32-byte row segments) and four thread
 // groups sharing the source tile for the production sizes; narrower tiles for large digit
 // counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches whose groups all
-// have the same source count 1..9 use the compile-time-K kernel.
+// have the same source count 1..12 use the compile-time-K kernel.
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   constexpr int NCOL = 1 << L2;
@@ -641,6 +642,7 @@ static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax
       switch (kmax) {
 #define LF_BC_K(K) case K: return launch_bc<L1, L2, CW8, 16, TG, K>(ctx, A, batch, kmax, s);
         LF_BC_K(1) LF_BC_K(2) LF_BC_K(3) LF_BC_K(4) LF_BC_K(5) LF_BC_K(6) LF_BC_K(7) LF_BC_K(8) LF_BC_K(9)
+        LF_BC_K(10) LF_BC_K(11) LF_BC_K(12)
 #undef LF_BC_K
         default: break;
       }
@@ -697,9 +699,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   {
     dim3 grid(l1 * groups, 1, nsh);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, 1, 0, -1); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, 1, 0, -1); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -770,41 +772,45 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   return 0;
 }
 
+// rescale by the top `nd` primes (1: ckks.rescale, ckks.py:220-225 / poly.py:284-287; 2: two
+// successive rescales fused into one floor division by q_l q_{l-1}, bit-identical since
+// floor(floor(X/a)/b) = floor(X/(ab)) for the exact representative X >= 0).
 template <int L1, int L2>
-static int rescale_pipeline(const LfCtx* ctx, int level, const u32* ct, size_t ct_bs, u32* out,
-                            size_t out_bs, int batch, void* ws, cudaStream_t s) {
+static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, size_t ct_bs,
+                            u32* out, size_t out_bs, int batch, void* ws, cudaStream_t s) {
   using S = NttShape<L1, L2>;
   const LfKsPlan* P = ctx->ks;
   const KsLevelPlan& K = P->lv[level];
   const int l = level;
+  const int nt = l + 1 - nd;                    // kept rows
   const size_t N = ctx->N;
   const LfDev dv = ctx->dev();
   const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
-  u32* T2 = (u32*)ws;                      // per instance: 2 rows, then T3: 2 l rows
-  const size_t per = (2 + 2 * (size_t)l) * N;
-  u32* T3 = T2 + 2 * N;
-  {  // row pass of INTT(b_l), INTT(a_l)  (poly.py:284-287 -> mod_down of the top prime)
-    dim3 grid(2 * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2, dv, l + 1, l, l); }
+  u32* T2 = (u32*)ws;                      // per instance: 2 nd rows, then T3: 2 nt rows
+  const size_t per = (2 * (size_t)nd + 2 * (size_t)nt) * N;
+  u32* T3 = T2 + 2 * (size_t)nd * N;
+  {  // row pass of INTT of the dropped rows of b and a
+    dim3 grid(2 * nd * groups, 1, batch);
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt); }
     LF_CHECK_LAUNCH();
   }
   {
     BcArgs A{};
     A.src = T2; A.dst = T3; A.src_bs = per; A.dst_bs = per;
     A.ngroups = 2;
-    A.g[0] = K.resc[0];
-    A.g[1] = K.resc[1];
-    A.tsplit = bc_tsplit(2, batch, (1 << L2) / 8, l);
-    if (int e = launch_bc_auto<L1, L2>(ctx, A, batch, 1, s)) return e;
+    A.g[0] = nd == 1 ? K.resc[0] : K.resc2[0];
+    A.g[1] = nd == 1 ? K.resc[1] : K.resc2[1];
+    A.tsplit = bc_tsplit(2, batch, (1 << L2) / 8, nt);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, batch, nd, s)) return e;
   }
   {
     ModDownArgs A{};
     A.T3 = T3; A.acc = ct; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
     A.t3_bs = per; A.acc_bs = ct_bs; A.out_bs = out_bs; A.e_bs = 0;
-    A.scal = P->qinv + (size_t)l * P->n_main * 2; A.sstride = 2;
-    A.nt = l; A.nacc = l + 1; A.ne = 0;
-    dim3 grid(l * groups, 1, batch);
+    A.scal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)l * P->n_main * 2; A.sstride = 2;
+    A.nt = nt; A.nacc = l + 1; A.ne = 0;
+    dim3 grid(nt * groups, 1, batch);
     { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
   }
@@ -824,7 +830,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, 1, 0, -1); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -995,7 +1001,19 @@ int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstri
   if (int e = ks_check(ctx, level)) return e;
   if (level < 1) { lf_set_error("rescale at level 0"); return 2; }
   if (!ct || !out || !workspace) { lf_set_error("lf_rescale: null argument"); return 1; }
-#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, 1, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_RS)
+#undef LF_RS
+  return 0;
+}
+
+int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct, size_t ct_bstride,
+                     uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (ndrop < 1 || ndrop > 2) { lf_set_error("lf_rescale_multi: ndrop %d not in {1, 2}", ndrop); return 2; }
+  if (level < ndrop) { lf_set_error("rescale by %d primes at level %d", ndrop, level); return 2; }
+  if (!ct || !out || !workspace) { lf_set_error("lf_rescale_multi: null argument"); return 1; }
+#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ndrop, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
   LF_DISPATCH_LOGN(ctx->logN, LF_RS)
 #undef LF_RS
   return 0;

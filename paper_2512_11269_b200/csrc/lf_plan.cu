@@ -157,6 +157,16 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
       qinv[((size_t)l * n_main + t) * 2 + 1] = shoupc(v, q);
     }
   const size_t off_qinv = blob.push(qinv);
+  // (q_l q_{l-1})^-1 mod q_t for the fused double rescale (two successive rescales,
+  // ckks.py:220-225, equal one floor division by q_l q_{l-1})
+  std::vector<u32> qinv2((size_t)n_main * n_main * 2, 0);
+  for (int l = 2; l <= L; ++l)
+    for (int t = 0; t < l - 1; ++t) {
+      const u32 q = primes[t], v = invm(mulm(primes[l] % q, primes[l - 1] % q, q), q);
+      qinv2[((size_t)l * n_main + t) * 2] = v;
+      qinv2[((size_t)l * n_main + t) * 2 + 1] = shoupc(v, q);
+    }
+  const size_t off_qinv2 = blob.push(qinv2);
 
   // ModDown table: specials -> main 0..L, y-multiplier folds the INTT's N^-1.
   std::vector<int> sp_src, main_all;
@@ -170,7 +180,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
     int beta, ext;
     TabRec up[LF_MAXD];
     size_t src_off[LF_MAXD], dst_off[LF_MAXD];
-    TabRec resc;
+    TabRec resc, resc2;
   };
   std::vector<LvRec> lvr(L + 1);
   for (int l = 0; l <= L; ++l) {
@@ -201,6 +211,11 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
       for (int t = 0; t < l; ++t) tgt.push_back(t);
       R.resc = build_table(blob, primes, src, tgt, {ninv[l]});
     }
+    if (l >= 2) {
+      std::vector<int> src{l - 1, l}, tgt;
+      for (int t = 0; t < l - 1; ++t) tgt.push_back(t);
+      R.resc2 = build_table(blob, primes, src, tgt, {ninv[l - 1], ninv[l]});
+    }
   }
 
   void* dmem = nullptr;
@@ -221,6 +236,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
   P->iota = (const int*)(base + off_iota);
   P->rowk = base + off_rowk;
   P->qinv = base + off_qinv;
+  P->qinv2 = base + off_qinv2;
   P->down = view(down);
   P->lv.resize(L + 1);
   for (int l = 0; l <= L; ++l) {
@@ -243,6 +259,15 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
         K.resc[p].dst_rows = P->iota;
         K.resc[p].src_row0 = p;
         K.resc[p].dst_row0 = p * l;
+      }
+    }
+    if (l >= 2) {
+      for (int p = 0; p < 2; ++p) {
+        K.resc2[p].B = view(R.resc2);
+        K.resc2[p].src_rows = P->iota;
+        K.resc2[p].dst_rows = P->iota;
+        K.resc2[p].src_row0 = 2 * p;
+        K.resc2[p].dst_row0 = p * (l - 1);
       }
     }
   }

@@ -22,6 +22,7 @@ struct KsLevelPlan {
   int level, beta, ext;
   BcGroupDev up[LF_MAXD];      // ModUp conversion of digit j (sources G_j, targets ext \ G_j)
   BcGroupDev resc[2];          // rescale at this level: q_level -> q_0..q_{level-1} (b and a)
+  BcGroupDev resc2[2];         // double rescale: {q_{level-1}, q_level} -> q_0..q_{level-2}
 };
 
 struct LfKsPlan {
@@ -31,6 +32,7 @@ struct LfKsPlan {
   const int* iota;                 // device 0..max(n_main, n_special) identity row list
   const u32* rowk;                 // [n_main][4]: s_t, s_t' (own-digit decomposition scalar), P^-1, P^-1'
   const u32* qinv;                 // [n_main][n_main][2]: q_l^-1 mod q_t and Shoup companion
+  const u32* qinv2;                // [n_main][n_main][2]: (q_l q_{l-1})^-1 mod q_t, companion
   void* dmem;
 };
 

@@ -89,6 +89,18 @@ def rescale(params, ct):
     return _pair(out, main_ids(level - 1))
 
 
+def rescale_multi(params, ct, ndrop: int):
+    """Drop the top `ndrop` (1 or 2) primes in one pass; ndrop=2 equals two rescales."""
+    ctx = get_context(params)
+    level = ct.level
+    ws = ctx.rescale_workspace(level)
+    c = ct_block(ct)
+    out = torch.empty((2, level + 1 - ndrop, params.N), dtype=torch.int32, device=c.device)
+    _native.check(_native.lib().lf_rescale_multi(ctx.handle, level, ndrop, dptr(c), 0, dptr(out), 0, 1,
+                                                 dptr(ws), stream_handle()), "lf_rescale_multi")
+    return _pair(out, main_ids(level - ndrop))
+
+
 def decompose(params, x: RnsPolynomial):
     ctx = get_context(params)
     level = len(x.basis_ids) - 1

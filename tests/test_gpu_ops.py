@@ -217,3 +217,21 @@ def test_batched_keyswitch_matches_single(B, golden_params):
         kb, ka = B.keyswitch(B.RnsPolynomial(xs[i], B.Domain.EVAL, tuple(range(l1))), rlk, p)
         assert np.array_equal(out[i, 0].cpu().numpy(), kb.limbs.cpu().numpy())
         assert np.array_equal(out[i, 1].cpu().numpy(), ka.limbs.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["desk", "c2"])
+def test_double_rescale_equals_two_rescales(B, golden_params, name):
+    """lf_rescale_multi(ndrop=2) == rescale(rescale(ct)) bit for bit (floor(floor(X/a)/b) =
+    floor(X/ab)); used by the bootstrap's double-prime levels."""
+    from paper_2512_11269_b200 import fused
+    p = B.gen_params(**golden_params[name]["kwargs"])
+    sk, pk, rlk = B.keygen(p, seed=3)
+    for level in (p.max_level, 2):
+        ids = tuple(range(level + 1))
+        rng = np.random.default_rng(level)
+        rows = lambda: np.stack([rng.integers(0, p.rns_basis[i], p.N, dtype=np.uint64) for i in ids])
+        E = B.Domain.EVAL
+        ct = B.Ciphertext(B.RnsPolynomial(rows(), E, ids), B.RnsPolynomial(rows(), E, ids), p.scale, level)
+        want = B.rescale(B.rescale(ct, p), p)
+        b, a = fused.rescale_multi(p, ct, 2)
+        assert np.array_equal(b.numpy(), want.b.numpy()) and np.array_equal(a.numpy(), want.a.numpy())

@@ -43,3 +43,37 @@ for _ in range(reps):
     torch.cuda.synchronize()
     ms.append((a.elapsed_time(b), (time.perf_counter() - w0) * 1e3))
 print("eager bootstrap ms (device, wall):", [(round(x, 2), round(y, 2)) for x, y in ms])
+
+if "--profile" in sys.argv:
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        out = bt.bootstrap(ct)
+        torch.cuda.synchronize()
+    ka = prof.key_averages()
+    tot = sum(k.device_time_total for k in ka)
+    print(f"kernel time total {tot / 1e3:.2f} ms over {sum(k.count for k in ka)} launches")
+    print(ka.table(sort_by="device_time_total", row_limit=15))
+
+if "--graph" in sys.argv:
+    static_in = ct
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        bt.bootstrap(static_in)
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        gout = bt.bootstrap(static_in)
+    g.replay()
+    torch.cuda.synchronize()
+    dg = B.decrypt(gout, sk, p)
+    print("graph output matches eager:", np.array_equal(gout.b.numpy(), out.b.numpy()))
+    ms = []
+    for _ in range(reps + 2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    print("graph bootstrap ms:", [round(x, 2) for x in ms])
