@@ -198,6 +198,95 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------------------
+C3 = dict(N=65536, num_levels=47, d=4, seed=0, scale=2 ** 26)
+
+
+def bootstrap_latency(reps=5):
+    """C3 variant ("Same p as C2 or a builder-tuned variant"): N=2^16, 48 main +
+    12 special primes, d=4, h=64.  Full-slot (n=2^15) bootstrap of a level-0 encryption of
+    uniform(-1,1) slots (seed 77), captured once as a CUDA graph and replayed; latency = CUDA
+    events around the replay (the graph holds every kernel of the pipeline; keys and
+    plaintext diagonals are resident).  Precision: max |decrypt(out) - decrypt(in)| in bits."""
+    import torch
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import bootstrap as BT
+    t0 = time.time()
+    p = B.gen_params(**C3)
+    sk, pk, rlk = B.keygen(p, seed=11)
+    cfg = BT.BootConfig()
+    planner = BT.Bootstrapper(type("P", (), {"N": p.N, "main_primes": p.rns_basis}), cfg)
+    ck, rk = BT.make_bootstrap_keys(p, sk, planner.required_rotations(), seed=99)
+    v = np.random.default_rng(77).uniform(-1, 1, p.n)
+    ct = B.encrypt(B.encode(v, p, level=0, scale=2 ** 26), pk, p, np.random.default_rng(5))
+    bt = BT.Bootstrapper(BT.GpuBackend(p, rlk, ck, rk), cfg)
+    out = bt.bootstrap(ct)                   # encodes and caches the plaintext diagonals
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    bt.bootstrap(ct)
+    e1.record()
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1)
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        bt.bootstrap(ct)
+    torch.cuda.current_stream().wait_stream(side)
+    with torch.cuda.graph(g):
+        gout = bt.bootstrap(ct)
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    assert np.array_equal(gout.b.numpy(), out.b.numpy()), "graph replay differs from eager"
+    din, dout = B.decrypt(ct, sk, p), B.decrypt(gout, sk, p)
+    err = float(np.abs(dout - din).max())
+    err_v = float(np.abs(dout - v).max())
+    return {"ms": statistics.median(ms), "ms_eager": eager_ms, "reps": reps,
+            "params": "gen_params(65536, 47, d=4, scale=2^26), h=64, full slots n=2^15",
+            "levels": f"in 0 -> out {gout.level} (L=47)", "precision_bits": -np.log2(err),
+            "max_err_vs_plain": err_v, "rotation_keys": len(rk) + 1,
+            "paper_1xB200_ms": 14.5, "setup_s": time.time() - t0}
+
+
+def sharded_keyswitch_latency(params, level, rlk, rank, world, dev, reps=10):
+    """one C2 keyswitch limb-sharded over all ranks (row bid on rank bid % k; one
+    all-gather before the ModUp base conversion, one before ModDown).  Latency = max over ranks
+    of the CUDA-event time of `reps` back-to-back sharded keyswitches (barrier on both sides)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_11269_b200.shard import Layout, TorchComm, gpu_sharded_keyswitch
+    comm = TorchComm()
+    lay = Layout(level, params.num_special, params.ks.d, world, rank)
+    q = torch.tensor([params.rns_basis[i] for i in lay.main_loc], dtype=torch.int64, device=dev)[:, None]
+    g = torch.Generator(device=dev).manual_seed(99)
+    x_loc = (torch.randint(0, 2 ** 62, (len(lay.main_loc), params.N), device=dev, generator=g,
+                           dtype=torch.int64) % q).to(torch.int32)
+    for _ in range(2):
+        gpu_sharded_keyswitch(params, level, x_loc, rlk, comm)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        gpu_sharded_keyswitch(params, level, x_loc, rlk, comm)
+    b.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    bytes_gathered = (level + 1 + 2 * params.num_special) * params.N * 4
+    return {"ms_per_keyswitch": float(t.item()), "ranks": world, "backend": comm.backend,
+            "allgather_rows": level + 1 + 2 * params.num_special,
+            "allgather_bytes_total": bytes_gathered,
+            "path": "shard.gpu_sharded_keyswitch (row kernels + 2 all-gathers; not the fused pipeline)"}
+
+
 def run_ours(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -316,6 +405,16 @@ def run_ours(args, rank, world):
         cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "port",
                "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
 
+    sharded = None
+    if world > 1:
+        sharded = sharded_keyswitch_latency(params, level, rlk, rank, world, dev)
+
+    boot = None
+    if rank == 0 and world == 1 and not args.no_bootstrap:
+        del xs, out, ws, flush
+        torch.cuda.empty_cache()
+        boot = bootstrap_latency()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world,
@@ -338,6 +437,8 @@ def run_ours(args, rank, world):
                     "api": "paper_2512_11269_b200.keyswitch per ciphertext"},
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "bootstrap": boot,
+            "limb_sharded": sharded,
         }
         print(json.dumps(line), flush=True)
 
@@ -351,6 +452,7 @@ def main():
     ap.add_argument("--level", type=int, default=35)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-bootstrap", action="store_true", help="skip the C3 bootstrap latency")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -358,11 +460,15 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LF_DIST_BACKEND", "nccl")     # gloo: several ranks on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
