@@ -122,49 +122,56 @@ LF_DEV void stage_flat(uint2* dst, const uint2* __restrict__ tab, int tid, int n
 }
 
 // Forward CT sub-transform of 2^K registers.  Input bound BIN (units of q).  DOFF = depth of
-// `root` below the line root.
+// `root` below the line root.  Stages are instantiated one by one (template recursion) so every
+// register index is a compile-time constant: a runtime-bounded inner loop would make nvcc demote
+// the register array to local memory.
+template <int K, int k, int BIN, int DOFF, class TW>
+LF_DEV void ct_stage(u32* x, u32 root, const TW& tw, u32 q) {
+  constexpr int h = 1 << (K - 1 - k);
+  constexpr bool corr = (fwd_corr_mask(BIN, K) >> k) & 1u;
+#pragma unroll
+  for (int blk = 0; blk < (1 << k); ++blk) {
+    const uint2 w = tw.get(DOFF + k, (root << k) + blk);
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      u32 X = x[blk * 2 * h + j];
+      const u32 Y = x[blk * 2 * h + h + j];
+      if (corr) X = csub(X, 8 * q);
+      const u32 t = mul_shoup_lazy(Y, w.x, w.y, q);
+      x[blk * 2 * h + j] = X + t;
+      x[blk * 2 * h + h + j] = X - t + 2 * q;
+    }
+  }
+  if constexpr (k + 1 < K) ct_stage<K, k + 1, BIN, DOFF>(x, root, tw, q);
+}
+
 template <int K, int BIN, int DOFF = 0, class TW>
 LF_DEV void ct_sub(u32* x, u32 root, const TW& tw, u32 q) {
   static_assert(BIN <= 16, "input bound too large");
-  constexpr unsigned CORR = fwd_corr_mask(BIN, K);
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int h = 1 << (K - 1 - k);
-    const bool corr = (CORR >> k) & 1u;
-#pragma unroll
-    for (int blk = 0; blk < (1 << k); ++blk) {
-      const uint2 w = tw.get(DOFF + k, (root << k) + blk);
-#pragma unroll
-      for (int j = 0; j < h; ++j) {
-        u32 X = x[blk * 2 * h + j];
-        const u32 Y = x[blk * 2 * h + h + j];
-        if (corr) X = csub(X, 8 * q);
-        const u32 t = mul_shoup_lazy(Y, w.x, w.y, q);
-        x[blk * 2 * h + j] = X + t;
-        x[blk * 2 * h + h + j] = X - t + 2 * q;
-      }
-    }
-  }
+  if constexpr (K > 0) ct_stage<K, 0, BIN, DOFF>(x, root, tw, q);
 }
 
 // Inverse GS sub-transform of 2^K registers, Harvey butterflies, [0,2q) in and out.
-template <int K, int DOFF = 0, class TW>
-LF_DEV void gs_sub(u32* x, u32 root, const TW& tw, u32 q) {
+template <int K, int k, int DOFF, class TW>
+LF_DEV void gs_stage(u32* x, u32 root, const TW& tw, u32 q) {
+  constexpr int h = 1 << (K - 1 - k);
 #pragma unroll
-  for (int k = K - 1; k >= 0; --k) {
-    const int h = 1 << (K - 1 - k);
+  for (int blk = 0; blk < (1 << k); ++blk) {
+    const uint2 w = tw.get(DOFF + k, (root << k) + blk);
 #pragma unroll
-    for (int blk = 0; blk < (1 << k); ++blk) {
-      const uint2 w = tw.get(DOFF + k, (root << k) + blk);
-#pragma unroll
-      for (int j = 0; j < h; ++j) {
-        const u32 X = x[blk * 2 * h + j];
-        const u32 Y = x[blk * 2 * h + h + j];
-        x[blk * 2 * h + j] = csub(X + Y, 2 * q);
-        x[blk * 2 * h + h + j] = mul_shoup_lazy(X - Y + 2 * q, w.x, w.y, q);
-      }
+    for (int j = 0; j < h; ++j) {
+      const u32 X = x[blk * 2 * h + j];
+      const u32 Y = x[blk * 2 * h + h + j];
+      x[blk * 2 * h + j] = csub(X + Y, 2 * q);
+      x[blk * 2 * h + h + j] = mul_shoup_lazy(X - Y + 2 * q, w.x, w.y, q);
     }
   }
+  if constexpr (k > 0) gs_stage<K, k - 1, DOFF>(x, root, tw, q);
+}
+
+template <int K, int DOFF = 0, class TW>
+LF_DEV void gs_sub(u32* x, u32 root, const TW& tw, u32 q) {
+  if constexpr (K > 0) gs_stage<K, K - 1, DOFF>(x, root, tw, q);
 }
 
 // Output bound (units of q) of a full forward line with input bound BIN.
