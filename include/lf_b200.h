@@ -132,6 +132,14 @@ int lf_rotate_hoisted(const lf_ctx* ctx, int level, const uint32_t* ct, int n_ro
                       const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
                       size_t out_bstride, void* workspace, void* stream);
 
+/* n independent rotations, each with its own ciphertext (ct_bstride words apart), Galois
+ * element gs[r] and key keys[r] (host array of device pointers): n separate lf_rotate calls in
+ * one pipeline (the giant steps of a BSGS linear transform).  Workspace:
+ * lf_ks_workspace_bytes(ctx, level, min(n, 64)). */
+int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
+                    const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                    size_t out_bstride, void* workspace, void* stream);
+
 /* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,

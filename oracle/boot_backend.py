@@ -100,6 +100,15 @@ class OracleBackend:
         return [x if s % self.P.n == 0 else O.hom_rotate(self.P, x, s, self.rk[s % self.P.n])
                 for x, s in zip(xs, steps)]
 
+    def bsgs_combine(self, groups):
+        acc = None
+        for st, pairs in groups:
+            c = self.mul_plain_sum(pairs)
+            if st % self.P.n:
+                c = O.hom_rotate(self.P, c, st, self.rk[st % self.P.n])
+            acc = c if acc is None else O.hom_add(self.P, acc, c)
+        return acc
+
     def mul_plain_sum(self, pairs):
         acc = None
         for c, pt in pairs:

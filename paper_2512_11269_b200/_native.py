@@ -56,6 +56,9 @@ def _load():
         "lf_rotate_hoisted": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
                                              ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
                                              ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_rotate_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int,
+                                           _u32_host, ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
         "lf_rescale_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                       ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),

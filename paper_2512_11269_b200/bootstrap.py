@@ -360,8 +360,8 @@ class Bootstrapper:
         S_p = Fraction(S_p)
         rots = be.rotate_hoisted(ct, plan.baby)
         rmap = dict(zip(plan.baby, rots))
-        inners = []
-        for k in sorted(plan.giants):
+        groups = []
+        for k in sorted(plan.giants, key=lambda k: (k != 0, k)):   # the unrotated giant first
             terms = plan.giants[k]
             pairs = []
             for b in plan.baby:
@@ -369,11 +369,8 @@ class Bootstrapper:
                 if bu in terms:
                     pt = self._pt((tag, k, bu), terms[bu] * const, l, S_p)
                     pairs.append((rmap[b], pt))
-            inners.append((k, be.mul_plain_sum(pairs)))
-        giant_steps = [(k * plan.g * plan.unit) % self.n for k, _ in inners]
-        acc = None
-        for c in be.rotate_many([c for _, c in inners], giant_steps):
-            acc = c if acc is None else be.add(acc, c)
+            groups.append(((k * plan.g * plan.unit) % self.n, pairs))
+        acc = be.bsgs_combine(groups)
         return be.rescale2(acc) if nres == 2 else be.rescale(acc)
 
     def _match(self, ct, level, scale):
@@ -679,7 +676,40 @@ class GpuBackend:
                 self.C.hom_rotate(x, s, self.rk[s % self.params.n], self.params)
                 for x, s in zip(xs, steps)]
 
-    def mul_plain_sum(self, pairs):
+    def bsgs_combine(self, groups):
+        """sum_k rot_{s_k}(sum_b ct_b * pt_{k,b}): the plaintext sums of all giant steps land in
+        one batch tensor, the rotated ones go through one batched rotation pipeline
+        (lf_rotate_batch), and the results are added in one linear-combination launch."""
+        import torch
+        from . import fused
+        from .poly import Domain, RnsPolynomial, main_ids
+        ct0 = groups[0][1][0][0]
+        level = ct0.level
+        N = self.params.N
+        n = len(groups)
+        inner = torch.empty((n, 2, level + 1, N), dtype=torch.int32, device=ct0.b.limbs.device)
+        for i, (_, pairs) in enumerate(groups):
+            self.mul_plain_sum(pairs, out=inner[i])
+        scale = ct0.scale * groups[0][1][0][1].scale
+        ids = main_ids(level)
+        rot_idx = [i for i, (st, _) in enumerate(groups) if st % self.params.n]
+        parts = [inner[i] for i, (st, _) in enumerate(groups) if st % self.params.n == 0]
+        if rot_idx:
+            lo, hi = rot_idx[0], rot_idx[-1] + 1
+            assert rot_idx == list(range(lo, hi)), "rotated giants must be contiguous"
+            gs = [galois_element_of(N, groups[i][0]) for i in rot_idx]
+            keys = [self.rk[groups[i][0] % self.params.n] for i in rot_idx]
+            rot = fused.rotate_batch(self.params, level, inner[lo:hi], gs, keys)
+            parts.extend(rot[j] for j in range(hi - lo))
+        cts = [self.C.Ciphertext(RnsPolynomial(p[0], Domain.EVAL, ids), RnsPolynomial(p[1], Domain.EVAL, ids),
+                                 scale, level) for p in parts]
+        acc = cts[0]
+        if len(cts) > 1:
+            acc = self.lincomb([(c, 1.0, Fraction(1)) for c in cts])
+            acc = self.C.Ciphertext(acc.b, acc.a, scale, level)
+        return acc
+
+    def mul_plain_sum(self, pairs, out=None):
         import torch
         from . import _native
         from .context import get_context, stream_handle
@@ -687,7 +717,8 @@ class GpuBackend:
         ct0, pt0 = pairs[0]
         level = ct0.level
         N = self.params.N
-        out = torch.empty((2, level + 1, N), dtype=torch.int32, device=ct0.b.limbs.device)
+        if out is None:
+            out = torch.empty((2, level + 1, N), dtype=torch.int32, device=ct0.b.limbs.device)
         ctx = get_context(self.params)
         lib = _native.lib()
         for i in range(0, len(pairs), 32):
@@ -701,7 +732,7 @@ class GpuBackend:
             _native.check(lib.lf_ptmac(ctx.handle, ctypes_void_p(tgt.data_ptr()), level + 1, n,
                                        bp, ap, pp, stream_handle()), "lf_ptmac")
             if i:
-                out = torch.stack([self._addrows(out[0], tgt[0], level), self._addrows(out[1], tgt[1], level)])
+                out.copy_(torch.stack([self._addrows(out[0], tgt[0], level), self._addrows(out[1], tgt[1], level)]))
         ids = main_ids(level)
         scale = ct0.scale * pt0.scale
         return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
@@ -755,6 +786,11 @@ class GpuBackend:
 
 
 from ctypes import c_void_p as ctypes_void_p  # noqa: E402
+
+
+def galois_element_of(N: int, steps: int) -> int:
+    from .ntt_host import galois_element
+    return galois_element(N, steps % (N // 2))
 
 
 def make_bootstrap_keys(params, sk, rotations, seed: int = 99):

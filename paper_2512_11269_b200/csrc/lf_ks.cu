@@ -1188,6 +1188,25 @@ int lf_rotate_hoisted(const lf_ctx* ctx, int level, const uint32_t* ct, int n_ro
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
 }
 
+int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
+                    const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                    size_t out_bstride, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!cts || !gs || !keys || !out || !workspace || n < 1) {
+    lf_set_error("lf_rotate_batch: bad argument");
+    return 1;
+  }
+  for (int r = 0; r < n; ++r)
+    if (!(gs[r] & 1) || !keys[r]) { lf_set_error("lf_rotate_batch: instance %d: bad key or even galois element", r); return 2; }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = n; c.op = OP_ROT; c.hoisted = false;
+  c.x = cts + arow; c.x2 = c.x; c.x_bs = ct_bstride; c.keylist = keys;
+  c.out = out; c.out_bs = out_bstride; c.e0 = cts; c.e1 = nullptr; c.e_bs = ct_bstride;
+  c.glist = gs;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
   if (!ctx) return 0;
   return (2 + 2 * (size_t)level) * ctx->N * 4 * (size_t)(batch < 1 ? 1 : batch);

@@ -78,6 +78,21 @@ def rotate_hoisted(params, ct, gs, keys):
     return [_pair(out[r], main_ids(level)) for r in range(n)]
 
 
+def rotate_batch(params, level: int, cts: torch.Tensor, gs, keys):
+    """cts: (n, 2, level+1, N) -> n rotations with their own Galois elements and keys."""
+    import ctypes
+    ctx = get_context(params)
+    n = cts.shape[0]
+    lib = _native.lib()
+    ws = ctx.ks_workspace(level, min(n, 64))
+    out = torch.empty_like(cts)
+    karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
+    _native.check(lib.lf_rotate_batch(ctx.handle, level, dptr(cts), cts[0].numel(), n, _native.u32_array(gs),
+                                      karr, dptr(out), out[0].numel(), dptr(ws), stream_handle()),
+                  "lf_rotate_batch")
+    return out
+
+
 def rescale(params, ct):
     ctx = get_context(params)
     level = ct.level

@@ -11,7 +11,9 @@ METRICS = [
     ("regs", "launch__registers_per_thread", 1),
     ("issue_active_%", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
     ("fma_pipe_%", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1),
-    ("fmaheavy_pipe_%", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", 1),
+    ("fmaheavy_pipe_%", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
+    ("l1tex_%", "l1tex__throughput.avg.pct_of_peak_sustained_active", 1),
+    ("smem_bank_confl", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1),
     ("alu_pipe_%", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 1),
     ("dram_%", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("warp_inst", "smsp__inst_executed.sum", 1),
