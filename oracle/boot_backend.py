@@ -13,6 +13,8 @@ from fractions import Fraction
 
 import numpy as np
 
+from paper_2512_11269_b200.bootstrap import ListBatch, map_batch
+
 from . import lf_oracle as O
 
 U64 = np.uint64
@@ -43,6 +45,9 @@ class OracleBackend:
         return self.P.main_ids(level)
 
     def drop_to_level(self, ct, level):
+        r = map_batch(self.drop_to_level, ct, level)
+        if r is not None:
+            return r
         if ct.level == level:
             return ct
         ids = self._ids(level)
@@ -67,20 +72,41 @@ class OracleBackend:
         return O.Plain(O.signed_to_eval(self.P, ints, self._ids(level)), Fraction(scale), level)
 
     def add(self, x, y):
+        r = map_batch(self.add, x, y)
+        if r is not None:
+            return r
         assert x.level == y.level and x.scale == y.scale
         return O.hom_add(self.P, x, y)
 
     def sub(self, x, y):
+        r = map_batch(self.sub, x, y)
+        if r is not None:
+            return r
         assert x.level == y.level and x.scale == y.scale
         return O.hom_sub(self.P, x, y)
 
     def rescale(self, x):
+        r = map_batch(self.rescale, x)
+        if r is not None:
+            return r
         return O.rescale(self.P, x)
 
     def rescale2(self, x):
+        r = map_batch(self.rescale2, x)
+        if r is not None:
+            return r
         return O.rescale(self.P, O.rescale(self.P, x))
 
+    def stack(self, cts):
+        return ListBatch(cts)
+
+    def unstack(self, x):
+        return list(x.cts)
+
     def lincomb(self, terms):
+        if isinstance(terms[0][0], ListBatch):
+            B = len(terms[0][0].cts)
+            return ListBatch([self.lincomb([(t.cts[i], c, S) for t, c, S in terms]) for i in range(B)])
         acc = None
         for ct, c, S in terms:
             t = self.mul_const(ct, c, S)
@@ -88,6 +114,9 @@ class OracleBackend:
         return acc
 
     def hom_mul(self, x, y):
+        r = map_batch(self.hom_mul, x, y)
+        if r is not None:
+            return r
         return O.hom_mul(self.P, x, y, self.rlk)
 
     def conjugate(self, x):
@@ -117,11 +146,17 @@ class OracleBackend:
         return acc
 
     def mul_const(self, ct, c, S_p):
+        r = map_batch(self.mul_const, ct, c, S_p)
+        if r is not None:
+            return r
         k = round(Fraction(c) * Fraction(S_p))
         sc = {b: k % self.P.prime(b) for b in ct.b.ids}
         return O.Ct(O.p_scale(self.P, ct.b, sc), O.p_scale(self.P, ct.a, sc), ct.scale * Fraction(S_p), ct.level)
 
     def add_const(self, ct, c):
+        r = map_batch(self.add_const, ct, c)
+        if r is not None:
+            return r
         k = round(Fraction(c) * Fraction(ct.scale))
         q = np.array([self.P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
         kk = np.array([k % self.P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]

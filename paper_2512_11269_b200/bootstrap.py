@@ -519,8 +519,7 @@ class Bootstrapper:
         im = be.mul_monomial(be.sub(x, xc), 3 * self.N // 2)   # * (-i) = * X^(3N/2)
         re = be.add_const(re, self.beta)
         im = be.add_const(im, self.beta)
-        re = self._evalmod(re)
-        im = self._evalmod(im)
+        re, im = be.unstack(self._evalmod(be.stack([re, im])))   # both parts in one batch
         y = be.add(re, be.mul_monomial(im, self.N // 2))       # re + i im
         # SlotToCoeff: the first level folds q0/Delta_in, the last lands on out_scale
         out_scale = Fraction(self.out_scale if out_scale is None else out_scale)
@@ -536,6 +535,32 @@ class Bootstrapper:
                 S_p = out_scale * q[l] * q[l - 1] / Fraction(y.scale)
                 y = self._linear(y, plan, tag, const, S_p, 2)
         return y
+
+
+class ListBatch:
+    """A batch of ciphertexts with one level and scale, executed one by one (backends without
+    batched kernels, e.g. the test oracle)."""
+
+    def __init__(self, cts):
+        self.cts = list(cts)
+        assert all(c.level == self.cts[0].level and c.scale == self.cts[0].scale for c in self.cts)
+        self.level, self.scale = self.cts[0].level, self.cts[0].scale
+
+
+class CtBatch:
+    """B ciphertexts at one level and scale in one (B, 2, level+1, N) device tensor; the GPU
+    backend runs every operation on all of them in one batched launch."""
+
+    def __init__(self, data, scale, level):
+        self.data, self.scale, self.level = data, Fraction(scale), level
+
+
+def map_batch(fn, *args):
+    """Apply a single-ciphertext op element-wise when the first argument is a ListBatch."""
+    if isinstance(args[0], ListBatch):
+        return ListBatch([fn(*[a.cts[i] if isinstance(a, ListBatch) else a for a in args])
+                          for i in range(len(args[0].cts))])
+    return None
 
 
 # ---------------------------------------------------------------------------------------
@@ -574,11 +599,29 @@ class GpuBackend:
         self.rk = rot_keys
         self._mono = {}
 
+    # batches (the two EvalMod evaluations run as one batch of 2 in every kernel)
+    def stack(self, cts):
+        import torch
+        return CtBatch(torch.stack([torch.stack([c.b.limbs, c.a.limbs]) for c in cts]),
+                       cts[0].scale, cts[0].level)
+
+    def unstack(self, x):
+        from .poly import Domain, RnsPolynomial, main_ids
+        ids = main_ids(x.level)
+        return [self.C.Ciphertext(RnsPolynomial(x.data[i, 0], Domain.EVAL, ids),
+                                  RnsPolynomial(x.data[i, 1], Domain.EVAL, ids), x.scale, x.level)
+                for i in range(x.data.shape[0])]
+
+    def _rows_pidx(self, x):
+        return tuple(range(x.level + 1)) * (2 * x.data.shape[0])
+
     # ciphertext plumbing
     def drop_to_level(self, ct, level):
         C = self.C
         if ct.level == level:
             return ct
+        if isinstance(ct, CtBatch):
+            return CtBatch(ct.data[:, :, : level + 1].contiguous(), ct.scale, level)
         assert level < ct.level
         from .poly import RnsPolynomial, main_ids
         ids = main_ids(level)
@@ -611,10 +654,25 @@ class GpuBackend:
         return Plaintext(signed_to_eval(ints, self.params, main_ids(level)), Fraction(scale), level)
 
     # arithmetic
+    def _b_ewise(self, op, x, y):
+        import torch
+        from .poly import ewise
+        assert x.level == y.level and x.scale == y.scale and x.data.shape == y.data.shape
+        out = torch.empty_like(x.data)
+        n = x.data.shape[0] * 2 * (x.level + 1)
+        ewise(self.params, op, out.view(n, -1), x.data.view(n, -1), self._rows_pidx(x), b=y.data.view(n, -1))
+        return CtBatch(out, x.scale, x.level)
+
     def add(self, x, y):
+        if isinstance(x, CtBatch):
+            from .poly import LF_OP_ADD
+            return self._b_ewise(LF_OP_ADD, x, y)
         return self.C.hom_add(x, y, self.params)
 
     def sub(self, x, y):
+        if isinstance(x, CtBatch):
+            from .poly import LF_OP_SUB
+            return self._b_ewise(LF_OP_SUB, x, y)
         return self.C.hom_sub(x, y, self.params)
 
     def rescale(self, x):
@@ -625,11 +683,37 @@ class GpuBackend:
         from . import fused
         if x.level < 2:
             raise ValueError("double rescale below level 2")
+        q = self.params.rns_basis
+        if isinstance(x, CtBatch):
+            import torch
+            from . import _native
+            from .context import dptr, get_context, stream_handle
+            ctx = get_context(self.params)
+            B = x.data.shape[0]
+            ws = ctx.rescale_workspace(x.level, B)
+            out = torch.empty((B, 2, x.level - 1, self.params.N), dtype=torch.int32, device=x.data.device)
+            _native.check(_native.lib().lf_rescale_multi(ctx.handle, x.level, 2, dptr(x.data), x.data[0].numel(),
+                                                         dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
+                          "lf_rescale_multi")
+            return CtBatch(out, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
         b, a = fused.rescale_multi(self.params, x, 2)
         q = self.params.rns_basis
         return self.C.Ciphertext(b, a, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
 
     def hom_mul(self, x, y):
+        if isinstance(x, CtBatch):
+            import torch
+            from . import _native
+            from .context import dptr, get_context, stream_handle
+            assert x.level == y.level and x.data.shape == y.data.shape and x.level >= 1
+            ctx = get_context(self.params)
+            B = x.data.shape[0]
+            ws = ctx.ks_workspace(x.level, B)
+            out = torch.empty_like(x.data)
+            _native.check(_native.lib().lf_hom_mul(ctx.handle, x.level, dptr(x.data), dptr(y.data), x.data[0].numel(),
+                                                   dptr(self.rlk.data), dptr(out), out[0].numel(), B, dptr(ws),
+                                                   stream_handle()), "lf_hom_mul")
+            return CtBatch(out, x.scale * y.scale, x.level)
         return self.C.hom_mul(x, y, self.rlk, self.params)
 
     def conjugate(self, x):
@@ -638,6 +722,10 @@ class GpuBackend:
     def lincomb(self, terms):
         """sum_i round(c_i S_i) * ct_i, all ct_i at one level with equal ct_i.scale * S_i."""
         import torch
+        if isinstance(terms[0][0], CtBatch):
+            B = terms[0][0].data.shape[0]
+            outs = [self.lincomb([(self.unstack(t)[i], c, S) for t, c, S in terms]) for i in range(B)]
+            return self.stack(outs)
         from . import _native
         from .context import get_context, stream_handle
         from .poly import Domain, RnsPolynomial, main_ids
@@ -754,6 +842,12 @@ class GpuBackend:
         k = round(Fraction(c) * Fraction(S_p))
         ids = main_ids(ct.level)
         sc = self._scalar_rows(ct, k)
+        if isinstance(ct, CtBatch):
+            n = ct.data.shape[0] * 2 * (ct.level + 1)
+            out = torch.empty_like(ct.data)
+            ewise(self.params, LF_OP_SCALAR_MUL, out.view(n, -1), ct.data.view(n, -1), self._rows_pidx(ct),
+                  scalars=sc * (2 * ct.data.shape[0]))
+            return CtBatch(out, ct.scale * Fraction(S_p), ct.level)
         out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
         ewise(self.params, LF_OP_SCALAR_MUL, out[0], ct.b.limbs, ids, scalars=sc)
         ewise(self.params, LF_OP_SCALAR_MUL, out[1], ct.a.limbs, ids, scalars=sc)
@@ -766,6 +860,14 @@ class GpuBackend:
         from .poly import LF_OP_ADD_SCALAR, Domain, RnsPolynomial, ewise, main_ids
         k = round(Fraction(c) * Fraction(ct.scale))
         ids = main_ids(ct.level)
+        if isinstance(ct, CtBatch):
+            B = ct.data.shape[0]
+            n = B * 2 * (ct.level + 1)
+            sc = (self._scalar_rows(ct, k) + [0] * (ct.level + 1)) * B       # b rows only
+            out = torch.empty_like(ct.data)
+            ewise(self.params, LF_OP_ADD_SCALAR, out.view(n, -1), ct.data.view(n, -1), self._rows_pidx(ct),
+                  scalars=sc)
+            return CtBatch(out, ct.scale, ct.level)
         out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
         ewise(self.params, LF_OP_ADD_SCALAR, out[0], ct.b.limbs, ids, scalars=self._scalar_rows(ct, k))
         out[1].copy_(ct.a.limbs)
