@@ -365,6 +365,13 @@ def run_ours(args, rank, world):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     ks_bytes = algorithmic_rows(level) * ROW_BYTES
     achieved_top = stage_info[top]["gbs"]
+    traffic = None            # ncu dram bytes of the same kernel, per launch (profiles/, committed)
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        if top in tr and Bsz == 8 and level == 35:
+            traffic = tr[top]["bytes_per_launch"]
+    except Exception:
+        pass
 
     # e2e: public API, pinned host inputs -> device -> keyswitch -> host, every step
     host_in = torch.empty((Bsz, l1, N), dtype=torch.int32, pin_memory=True)
@@ -428,8 +435,10 @@ def run_ours(args, rank, world):
             "keyswitch_hbm": {"algorithmic_bytes": ks_bytes, "achieved_gbs": ks_bytes * value / world / 1e9,
                               "peak_gbs": hbm_peak, "frac": ks_bytes * value / world / 1e9 / hbm_peak},
             "roofline": {"kernel": top, "bound": "hbm", "achieved": achieved_top, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": None,
-                         "peak_source": peak_src},
+                         "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": rows[top] * ROW_BYTES * Bsz,
+                         "peak_source": peak_src,
+                         "note": "algorithmic bytes / CUDA-event time of the launch; traffic = ncu dram read+write of the same launch (profiles/r01_ncu_traffic.json)"},
             "stages": stage_info,
             "gpu_launches": 5 * args.steps,
             "e2e": {"value": e2e_value, "unit": "ops/s",
