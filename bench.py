@@ -254,6 +254,36 @@ def bootstrap_latency(reps=5):
             "paper_1xB200_ms": 14.5, "setup_s": time.time() - t0}
 
 
+def ntt_throughput(params, dev, rows=720, reps=10):
+    """Standalone batched negacyclic NTT / INTT at N=2^16 over C2 primes ("integer-pipe
+    utilisation for the NTT").  720 rows (189 MB) > L2, so both passes stream from HBM.
+    Integer-pipe fraction: one Shoup IMAD.HI per butterfly and IMAD.HI issues at 32/clk/SM on
+    B200 (tools/ubench/imad.cu, profiles/r01_ubench_imad.log)."""
+    import torch
+    from paper_2512_11269_b200 import poly as P
+    ids = [i % (params.max_level + 1) for i in range(rows)]
+    q = torch.tensor([params.rns_basis[i] for i in ids], dtype=torch.int64, device=dev)[:, None]
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = (torch.randint(0, 2 ** 62, (rows, params.N), device=dev, generator=g, dtype=torch.int64) % q).to(torch.int32)
+    for _ in range(2):
+        P.ntt_rows(params, x, ids)
+        P.ntt_rows(params, x, ids, inverse=True)
+    torch.cuda.synchronize()
+    out = {}
+    bfly = rows * (params.N // 2) * (params.N.bit_length() - 1)
+    for name, inv in (("fwd", False), ("inv", True)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            P.ntt_rows(params, x, ids, inverse=inv)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        out[name] = {"us": ms * 1e3, "butterflies_per_s": bfly / (ms * 1e-3),
+                     "hbm_gbs_two_passes": 4 * rows * params.N * 4 / (ms * 1e-3) / 1e9}
+    return out
+
+
 def sharded_keyswitch_latency(params, level, rlk, rank, world, dev, reps=10):
     """one C2 keyswitch limb-sharded over all ranks (row bid on rank bid % k; one
     all-gather before the ModUp base conversion, one before ModDown).  Latency = max over ranks
@@ -285,6 +315,16 @@ def sharded_keyswitch_latency(params, level, rlk, rank, world, dev, reps=10):
             "allgather_rows": level + 1 + 2 * params.num_special,
             "allgather_bytes_total": bytes_gathered,
             "path": "shard.gpu_sharded_keyswitch (row kernels + 2 all-gathers; not the fused pipeline)"}
+
+
+def ntt_summary(ntt, clocks):
+    mhz = (clocks or {}).get("sm_mhz") or 1965
+    peak = 32 * 148 * mhz * 1e6                  # IMAD.HI per second (one per butterfly)
+    for v in ntt.values():
+        v["imad_hi_frac"] = v["butterflies_per_s"] / peak
+    ntt["config"] = "720 rows x 2^16, C2 primes, lf_ntt_fwd / lf_ntt_inv (column + row pass)"
+    ntt["int_peak"] = f"32 IMAD.HI/clk/SM x 148 SMs x {mhz} MHz (measured rate, profiles/r01_ubench_imad.log)"
+    return ntt
 
 
 def run_ours(args, rank, world):
@@ -412,6 +452,8 @@ def run_ours(args, rank, world):
         cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "port",
                "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
 
+    ntt = ntt_throughput(params, dev)
+
     sharded = None
     if world > 1:
         sharded = sharded_keyswitch_latency(params, level, rlk, rank, world, dev)
@@ -447,6 +489,7 @@ def run_ours(args, rank, world):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "bootstrap": boot,
+            "ntt": ntt_summary(ntt, clocks),
             "limb_sharded": sharded,
         }
         print(json.dumps(line), flush=True)

@@ -195,13 +195,15 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
   const int c = lt % CW, tl = lt / CW;
   const int rot = c >> 1;
+  // blockIdx.x = ((group * NCT + ct) * nbatch + b) * tsplit + ts: the tsplit CTAs that share one
+  // (group, column tile, instance) are consecutive and form a thread-block cluster.
   int bid = blockIdx.x;
+  const int ts = bid % A.tsplit;
+  bid /= A.tsplit;
   const int b = bid % nbatch;
   bid /= nbatch;
   const int ct = bid % NCT;
-  const int gy = bid / NCT;
-  const BcGroupDev& G = A.g[gy / A.tsplit];
-  const int ts = gy % A.tsplit;
+  const BcGroupDev& G = A.g[bid / NCT];
   const BconvDev& B = G.B;
   const int k = KEX > 0 ? KEX : B.k;
   const int col = ct * CW + c;
@@ -218,8 +220,11 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
   for (int w = threadIdx.x; w < (t1 - t0) * k; w += blockDim.x) Wsm[w] = __ldg(&B.w[(size_t)t0 * k + w]);
 
-  // phase 1: INTT column pass of each source row (sources split over the groups)
-  for (int i = grp; i < k; i += TG) {
+  // phase 1: INTT column pass of each source row, sources split over the groups and (when the
+  // target range is split over a cluster) over the cluster's CTAs; the other CTAs' converted
+  // source tiles are then pulled through distributed shared memory instead of recomputed.
+  const int cl = A.tsplit;
+  for (int i = ts + cl * grp; i < k; i += cl * TG) {
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
@@ -230,6 +235,24 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     for (int j = 0; j < E; ++j) x[j] = mul_shoup(x[j], ci, cpi, pk.q);
     y_store<E>(Ybase + (size_t)i * YI, x, rot);
     gsync();
+  }
+  if (cl > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    for (int i = 0; i < k; ++i) {
+      const int r = i % cl;
+      if (r == ts) continue;
+      for (int v = threadIdx.x; v < YI / 4; v += blockDim.x) {
+        u32* loc = sm + (size_t)i * YI + 4 * v;
+        const unsigned la = (unsigned)__cvta_generic_to_shared(loc);
+        unsigned ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
+        uint4 q;
+        asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(ra) : "memory");
+        *reinterpret_cast<uint4*>(loc) = q;
+      }
+    }
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // done reading peers
   }
   __syncthreads();
 
@@ -295,6 +318,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
     gsync();
   }
+  if (cl > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // peers done with my tile
 }
 
 // ---------------------------------------------------------------------------------------
@@ -795,7 +819,25 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
   auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG, KEX>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const long nblocks = (long)batch * ((1 << L2) / CW) * A.ngroups * A.tsplit;
-  kern<<<(unsigned)nblocks, TG * CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax, batch);
+  if (A.tsplit > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nblocks);
+    cfg.blockDim = dim3(TG * CW * LineCfg<L1>::T);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = A.tsplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LfDev dv = ctx->dev();
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, dv, kmax, batch);
+    if (e != cudaSuccess) { lf_set_error("bconv cluster launch: %s", cudaGetErrorString(e)); return 3; }
+  } else {
+    kern<<<(unsigned)nblocks, TG * CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax, batch);
+  }
   LF_CHECK_LAUNCH();
   return 0;
 }
