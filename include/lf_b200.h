@@ -178,6 +178,11 @@ int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint3
 int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
                const uint32_t* const* a, const uint32_t* k, void* stream);
 
+/* LFHE wire rows (little-endian uint64, reference serial.py:1-14, 63-69) <-> device uint32
+ * residues, n words, both pointers on the device. */
+int lf_rows_from_u64(uint32_t* out, const uint64_t* in, size_t n, void* stream);
+int lf_rows_to_u64(uint64_t* out, const uint32_t* in, size_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

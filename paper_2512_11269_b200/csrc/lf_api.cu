@@ -209,4 +209,14 @@ int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uin
   return lf_launch_lincomb(ctx, out, nrows, nterm, b, a, k, (cudaStream_t)stream);
 }
 
+int lf_rows_from_u64(uint32_t* out, const uint64_t* in, size_t n, void* stream) {
+  if (!out || !in) { lf_set_error("lf_rows_from_u64: null argument"); return 1; }
+  return lf_launch_convert(out, in, n, true, (cudaStream_t)stream);
+}
+
+int lf_rows_to_u64(uint64_t* out, const uint32_t* in, size_t n, void* stream) {
+  if (!out || !in) { lf_set_error("lf_rows_to_u64: null argument"); return 1; }
+  return lf_launch_convert(out, in, n, false, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -196,6 +196,27 @@ int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u3
   return 0;
 }
 
+// Wire-format conversion (LFHE rows are little-endian uint64, serial.py:1-14): narrow to the
+// device's uint32 residues (values < 2^28) or widen back.
+__global__ void __launch_bounds__(256) k_narrow(u32* out, const unsigned long long* in, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (u32)in[i];
+}
+__global__ void __launch_bounds__(256) k_widen(unsigned long long* out, const u32* in, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStream_t s) {
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks == 0) return 0;
+  if (narrow) k_narrow<<<(unsigned)blocks, 256, 0, s>>>((u32*)out, (const unsigned long long*)in, n);
+  else k_widen<<<(unsigned)blocks, 256, 0, s>>>((unsigned long long*)out, (const u32*)in, n);
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
 int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
                        cudaStream_t s) {
   const size_t total = (size_t)ctx->N * nin * nout;

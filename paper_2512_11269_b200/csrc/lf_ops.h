@@ -19,3 +19,4 @@ int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32*
 #define LF_LINCOMB_ROWS 64
 int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
                       const u32* const* a, const u32* k, cudaStream_t s);
+int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStream_t s);
