@@ -16,6 +16,10 @@
 //                     [hom_mul: + d0/d1; rotate: + sigma_g(b)]            -> out (2 (l+1))
 // Every pass works on whole lines held in registers, so each intermediate row crosses HBM
 // (or L2) once per kernel boundary.  All kernels take a batch dimension (grid.z).
+// Intermediates T0..T3 are stored LINE-TRANSPOSED: inside each 2^L2-word line, element
+// p = tl + T*j (the row pass's step-1 order) lives at word tl*E + j, so the row kernels move
+// them with contiguous 16-byte accesses; the column kernels are layout-agnostic (every column
+// is transformed identically), they only see a permuted column order.
 #include "lf_ntt.cuh"
 #include "lf_bconv.cuh"
 #include "lf_plan.h"
@@ -26,6 +30,9 @@
 
 // Bulk L2 prefetch (TMA engine, sm_90+): warms the next stage's contiguous row segment so the
 // per-thread loads that follow hit L2 instead of HBM.  bytes must be a multiple of 16.
+LF_DEV void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 LF_DEV void prefetch_l2(const void* p, u32 bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -70,7 +77,7 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   __syncthreads();
   inv_line<L2>(v, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
                rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
-  store_row_step1<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)row << (L1 + L2)) +
+  store_row_step2<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)row << (L1 + L2)) +
                              ((size_t)hi << L2), tl);
 }
 
@@ -374,6 +381,19 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   int hi0s = (bl % groups) * S::LPCR;
   if (GALOIS)
     hi0s = (int)((auto_src_index((u32)hi0s << L2, gal, logN) >> L2) / S::LPCR) * S::LPCR;
+  // L1 prefetch of one digit's data for this thread (its 64-byte slices of the piece row and of
+  // the two key rows): issued one digit ahead so the loads at the top of the next iteration hit
+  // L1 instead of exposing the full HBM/L2 latency to the first butterfly.
+  const int own_j = is_main ? t % A.d : -1;
+  auto prefetch_digit = [&](int j) {
+    if (j >= A.beta) return;
+    const size_t lo = ((size_t)hi << L2) + (size_t)tl * C::E;
+    if (j != own_j)
+      prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
+    prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
+    prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
+  };
+  prefetch_digit(0);
   stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
                        threadIdx.x, blockDim.x);
   cp_async_wait_all();
@@ -383,24 +403,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
   for (int e = 0; e < C::E; ++e) { accb[e] = 0; acca[e] = 0; }
 
-  const int hi0 = (bl % groups) * S::LPCR;
-  constexpr u32 SEG = (u32)S::LPCR << L2;                     // words of this CTA's lines
-  auto prefetch_digit = [&](int j) {
-    if (threadIdx.x == 0 && j < A.beta) {
-      const size_t lo0 = (size_t)hi0 << L2;
-      if (!(is_main && (t % A.d) == j))
-        prefetch_l2(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + lo0, SEG * 4);
-      prefetch_l2(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo0, SEG * 4);
-      prefetch_l2(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo0, SEG * 4);
-    }
-  };
-  (void)prefetch_digit;
   for (int j = 0; j < A.beta; ++j) {
-    u32 kvb[C::E], kva[C::E];
-    load_row_step2<L2>(kvb, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
-    load_row_step2<L2>(kva, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
+    prefetch_digit(j + 1);
     u32 pc[C::E];
-    if (is_main && (t % A.d) == j) {
+    if (j == own_j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
       const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
       const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
@@ -415,7 +421,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       }
     } else {
       const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
-      load_row_step1<L2>(pc, tr, tl);
+      load_row_step2<L2>(pc, tr, tl);
       fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
                         tl, addr, SyncWarp{});
       if (GALOIS) {
@@ -433,10 +439,17 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e) pc[e] = reduce32_lazy(pc[e], pk);
     }
+    {
+      // key rows are loaded only now (L1-prefetched one digit ahead): keeping them live across
+      // the row NTT would push the kernel past 128 registers and spill the twiddle addresses
+      u32 kv[C::E];
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kvb[e];
+      for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kv[e];
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kva[e];
+      for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kv[e];
+    }
   }
   u32 rb[C::E], ra[C::E];
 #pragma unroll
@@ -449,10 +462,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     const uint2* tw = dv.twi + ((size_t)pi << logN);
     __syncwarp();
     inv_line<L2>(rb, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step1<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
     __syncwarp();
     inv_line<L2>(ra, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step1<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
   }
 }
 
@@ -564,8 +577,7 @@ k_ks_inner_pf(KsInnerArgs A, LfDev dv) {
       }
     } else {
       const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
-#pragma unroll
-      for (int e = 0; e < E; ++e) cp_async4(sp + slot_idx<E, NT>(e, tid), tr + tl + T * e);
+      slot_fill_contig<E, NT>(sp, tr + (size_t)tl * E, tid);        // line-transposed T1
     }
     cp_async_commit();
   };
@@ -638,10 +650,10 @@ k_ks_inner_pf(KsInnerArgs A, LfDev dv) {
     const uint2* twi = dv.twi + ((size_t)pi << logN);
     __syncwarp();
     inv_line<L2>(rb, (1u << L1) + hi, twi, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step1<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
     __syncwarp();
     inv_line<L2>(ra, (1u << L1) + hi, twi, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step1<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
   }
 }
 
@@ -686,7 +698,12 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
 #pragma unroll 1
   for (int p = 0; p < 2; ++p) {
     u32 cv[C::E], av[C::E];
-    load_row_step1<L2>(cv, A.T3 + b * A.t3_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
+    load_row_step2<L2>(cv, A.T3 + b * A.t3_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
+    if (p == 0) {     // the a-polynomial's rows arrive in L1 while the b-polynomial is processed
+      prefetch_l1(A.T3 + b * A.t3_bs + ((size_t)(A.nt + t) << logN) + lo0 + (size_t)tl * C::E);
+      prefetch_l1(A.acc + b * A.acc_bs + ((size_t)t << logN) + lo0 + (size_t)tl * C::E);
+      prefetch_l1(A.acc + b * A.acc_bs + ((size_t)(A.nacc + t) << logN) + lo0 + (size_t)tl * C::E);
+    }
     if (p) {
       __syncwarp();
     } else {
@@ -759,7 +776,7 @@ k_pieces(const u32* __restrict__ T1, const u32* __restrict__ x, u32* __restrict_
 #pragma unroll
     for (int e = 0; e < C::E; ++e) v[e] = mul_shoup(v[e], rowk[4 * t], rowk[4 * t + 1], pk.q);
   } else {
-    load_row_step1<L2>(v, T1 + ((size_t)r << logN) + lo0, tl);
+    load_row_step2<L2>(v, T1 + ((size_t)r << logN) + lo0, tl);
     fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi, dv.twf + ((size_t)pi << logN), pk.q,
                                rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
 #pragma unroll
