@@ -204,9 +204,10 @@ C3 = dict(N=65536, num_levels=47, d=4, seed=0, scale=2 ** 26)
 def bootstrap_latency(reps=5):
     """C3 variant ("Same p as C2 or a builder-tuned variant"): N=2^16, 48 main +
     12 special primes, d=4, h=64.  Full-slot (n=2^15) bootstrap of a level-0 encryption of
-    uniform(-1,1) slots (seed 77), captured once as a CUDA graph and replayed; latency = CUDA
-    events around the replay (the graph holds every kernel of the pipeline; keys and
-    plaintext diagonals are resident).  Precision: max |decrypt(out) - decrypt(in)| in bits."""
+    uniform(-1,1) slots (seed 77), captured once as a CUDA graph (bootstrap.GraphedBootstrap)
+    and replayed; latency = CUDA events around the call (input copy into the captured buffers,
+    replay, output copy; keys and plaintext diagonals are resident).  Precision:
+    max |decrypt(out) - decrypt(in)| in bits."""
     import torch
     import paper_2512_11269_b200 as B
     from paper_2512_11269_b200 import bootstrap as BT
@@ -227,19 +228,12 @@ def bootstrap_latency(reps=5):
     e1.record()
     torch.cuda.synchronize()
     eager_ms = e0.elapsed_time(e1)
-    g = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        bt.bootstrap(ct)
-    torch.cuda.current_stream().wait_stream(side)
-    with torch.cuda.graph(g):
-        gout = bt.bootstrap(ct)
+    graphed = BT.GraphedBootstrap(bt, ct)                 # public API: capture once, replay
     ms = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        g.replay()
+        gout = graphed(ct)
         b.record()
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))

@@ -102,10 +102,16 @@ def test_gpu_bootstrap_bit_exact_vs_oracle():
     ck, rk = BT.make_bootstrap_keys(p, sk, planner.required_rotations(), seed=99)
     ct = B.encrypt(B.encode(v, p, level=0, scale=2 ** 22), pk, p, np.random.default_rng(5))
     assert np.array_equal(ct.b.numpy(), ct_o.b.rows) and np.array_equal(ct.a.numpy(), ct_o.a.rows)
-    got = BT.Bootstrapper(BT.GpuBackend(p, rlk, ck, rk), TOY_CFG).bootstrap(ct)
+    bt = BT.Bootstrapper(BT.GpuBackend(p, rlk, ck, rk), TOY_CFG)
+    got = bt.bootstrap(ct)
     assert got.level == want.level and got.scale == want.scale
     assert np.array_equal(got.b.numpy(), want.b.rows)
     assert np.array_equal(got.a.numpy(), want.a.rows)
+    # the CUDA-graph replay of the same pipeline gives the same residues, also for a new input
+    g = BT.GraphedBootstrap(bt, ct)
+    assert np.array_equal(g(ct).b.numpy(), want.b.rows)
+    ct2 = B.encrypt(B.encode(-v, p, level=0, scale=2 ** 22), pk, p, np.random.default_rng(6))
+    assert np.array_equal(g(ct2).a.numpy(), bt.bootstrap(ct2).a.numpy())
 
 
 @pytest.mark.gpu
