@@ -183,6 +183,22 @@ int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uin
 int lf_rows_from_u64(uint32_t* out, const uint64_t* in, size_t n, void* stream);
 int lf_rows_to_u64(uint64_t* out, const uint32_t* in, size_t n, void* stream);
 
+/* Hoisted-ModDown building blocks for BSGS linear transforms: the same key switch as
+ * lf_rotate_hoisted, stopped before ModDown.  out_ext receives, per rotation r,
+ * 2 x (level+1+alpha) rows (extended basis, eval domain): (P*sigma_g(b) + acc_b, acc_a), the
+ * inner product of keyswitch_inner_product (ckks.py:120-131) over permuted pieces.
+ * lf_moddown_ext applies mod_down (poly.py:251-281) to both polynomials of such blocks. */
+int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                          const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                          size_t out_bstride, void* workspace, void* stream);
+size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch);
+int lf_moddown_ext(const lf_ctx* ctx, int level, const uint32_t* in_ext, size_t in_bstride,
+                   uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
+/* lf_ptmac over rows with arbitrary primes (prime_idx: HOST array, nrows entries). */
+int lf_ptmac_rows(const lf_ctx* ctx, uint32_t* out, int nrows, const int32_t* prime_idx, int nterm,
+                  const uint32_t* const* b, const uint32_t* const* a, const uint32_t* const* pt,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,9 +67,56 @@ class OracleBackend:
             out.append(O.Poly(rows, ids))
         return O.Ct(out[0], out[1], ct.scale, L)
 
-    def encode_slots(self, values, level, scale):
+    def encode_slots(self, values, level, scale, ext=False):
         ints = encode_ints(values, self.N, scale)
-        return O.Plain(O.signed_to_eval(self.P, ints, self._ids(level)), Fraction(scale), level)
+        ids = self.P.ext_ids(level) if ext else self._ids(level)
+        return O.Plain(O.signed_to_eval(self.P, ints, ids), Fraction(scale), level)
+
+    # hoisted ModDown: extended-basis ciphertexts as O.Ct over ext ids
+    def extend(self, ct):
+        P = self.P
+        ext = P.ext_ids(ct.level)
+        Pp = O.special_product(P)
+        q = np.array([P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+        s = np.array([Pp % P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+        z = np.zeros((P.alpha, P.N), dtype=U64)
+        b = O.Poly(np.concatenate([ct.b.rows * s % q, z]), ext)
+        a = O.Poly(np.concatenate([ct.a.rows * s % q, z]), ext)
+        return O.Ct(b, a, ct.scale, ct.level)
+
+    def rotate_hoisted_ext(self, ct, steps):
+        """keyswitch_decompose -> automorph -> keyswitch_inner_product (ckks.py:95-131), and
+        P * sigma_g(b) on the main rows: hom_rotate (ckks.py:197-217) before its mod_down."""
+        P = self.P
+        ext = P.ext_ids(ct.level)
+        Pp = O.special_product(P)
+        pieces = O.ks_decompose(P, ct.a)
+        out = []
+        for st in steps:
+            g = O.galois_element(P.N, st % P.n)
+            ab, aa = O.ks_inner(P, [(j, O.p_automorph(P, d, g)) for j, d in pieces], self.rk[st % P.n])
+            sb = O.p_automorph(P, ct.b, g)
+            q = np.array([P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+            s = np.array([Pp % P.prime(b) for b in ct.b.ids], dtype=U64)[:, None]
+            main = ab.rows[: ct.level + 1]
+            b = O.Poly(np.concatenate([(main + sb.rows * s % q) % q, ab.rows[ct.level + 1:]]), ext)
+            out.append(O.Ct(b, aa, ct.scale, ct.level))
+        return out
+
+    def bsgs_combine_ext(self, groups):
+        P = self.P
+        acc = None
+        for st, pairs in groups:
+            s = None
+            for x, pt in pairs:
+                t = O.Ct(O.p_mul(P, x.b, pt.poly), O.p_mul(P, x.a, pt.poly), x.scale * pt.scale, x.level)
+                s = t if s is None else O.hom_add(P, s, t)
+            ids = P.main_ids(s.level)
+            c = O.Ct(O.mod_down(P, s.b, ids), O.mod_down(P, s.a, ids), s.scale, s.level)
+            if st % P.n:
+                c = O.hom_rotate(P, c, st, self.rk[st % P.n])
+            acc = c if acc is None else O.hom_add(P, acc, c)
+        return acc
 
     def add(self, x, y):
         r = map_batch(self.add, x, y)

@@ -69,6 +69,15 @@ def _load():
                                       _u32_host, ctypes.c_void_p]),
         "lf_rows_from_u64": (ctypes.c_int, [_u32p, _u32p, ctypes.c_size_t, ctypes.c_void_p]),
         "lf_rows_to_u64": (ctypes.c_int, [_u32p, _u32p, ctypes.c_size_t, ctypes.c_void_p]),
+        "lf_rotate_hoisted_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
+                                                 ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
+                                                 ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_moddown_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+        "lf_moddown_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
+                                          ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_ptmac_rows": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, _i32_host, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                         ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
         "lf_ks_decompose": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, _u32p, ctypes.c_void_p,
                                            ctypes.c_void_p]),
         "lf_modraise": (ctypes.c_int, [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_int,

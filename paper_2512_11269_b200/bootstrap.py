@@ -191,7 +191,10 @@ class BsgsPlan:
         return r
 
 
-def bsgs_plan(M: DiagMat, n: int) -> BsgsPlan:
+def bsgs_plan(M: DiagMat, n: int, ratio: int = 1) -> BsgsPlan:
+    """Baby-step span g: the smallest power of two with g^2 >= span * ratio.  ratio > 1 favours
+    baby steps, right when a giant step costs `ratio` baby steps (hoisted ModDown: baby steps
+    skip ModDown, giant steps pay a ModDown plus a full rotation)."""
     offs = sorted(M)
     signed = [d if d <= n // 2 else d - n for d in offs]
     nz = [abs(s) for s in signed if s]
@@ -204,7 +207,7 @@ def bsgs_plan(M: DiagMat, n: int) -> BsgsPlan:
     ms = [s // unit for s in signed]
     span = max(ms) - min(ms) + 1
     g = 1
-    while g * g < span:
+    while g * g < span * ratio:
         g *= 2
     giants = {}
     babies = set()
@@ -268,6 +271,8 @@ class BootConfig:
     r: int = 3                   # double angles
     cheb_degree: int = 31
     baby: int = 8                # Chebyshev baby steps T_0..T_7
+    lazy_moddown: bool = True    # BSGS: one ModDown per giant step instead of per rotation
+    bsgs_ratio: int = 4          # giant/baby cost ratio used to size the baby steps
 
 
 def evalmod_constants(cfg: BootConfig):
@@ -322,8 +327,9 @@ class Bootstrapper:
         # given input slots z = Embed(t)/Delta_in; Delta_in varies, so the factor Delta_in/q0
         # is applied through the declared scale (see bootstrap()).  Balance the magnitude over
         # the levels so every diagonal is O(1) (plaintext precision).
-        self.cts_plans = [bsgs_plan(M, n) for M in cts]
-        self.stc_plans = [bsgs_plan(M, n) for M in stc]
+        ratio = cfg.bsgs_ratio if cfg.lazy_moddown else 1
+        self.cts_plans = [bsgs_plan(M, n, ratio) for M in cts]
+        self.stc_plans = [bsgs_plan(M, n, ratio) for M in stc]
         self.cts_const = self.alpha / 2
         self.rotations = set()
         for pl in self.cts_plans + self.stc_plans:
@@ -344,22 +350,35 @@ class Bootstrapper:
         return {"cts": self.cts_at, "evalmod_in": self.evalmod_in}
 
     # -- helpers ---------------------------------------------------------------------
-    def _pt(self, key, vec, level, scale):
-        k = (key, level, scale)
+    def _pt(self, key, vec, level, scale, ext=False):
+        k = (key, level, scale, ext)
         pt = self._pt_cache.get(k)
         if pt is None:
-            pt = self.be.encode_slots(vec, level, scale)
+            pt = self.be.encode_slots(vec, level, scale, ext=ext)
             self._pt_cache[k] = pt
         return pt
 
     def _linear(self, ct, plan: BsgsPlan, tag, const, S_p, nres: int):
         """sum_d diag_d * rot(ct, d) with BSGS: diagonals (times `const`) encoded at the
-        plaintext scale S_p, then `nres` rescales."""
+        plaintext scale S_p, then `nres` rescales.
+
+        Hoisted ModDown (cfg.lazy_moddown): the baby-step rotations share one ModUp and stop
+        before ModDown, (P sigma_b(b) + acc_b, acc_a) over the extended basis Q_l P
+        (keyswitch_inner_product, ckks.py:120-131); the identity step is P*ct.  Each giant
+        step multiplies them by its extended-basis diagonals, sums, and runs ONE mod_down
+        (poly.py:251-281) — instead of one per baby rotation.  The composition only uses
+        reference primitives, so the oracle backend reproduces it residue for residue."""
         be = self.be
         l = ct.level
         S_p = Fraction(S_p)
-        rots = be.rotate_hoisted(ct, plan.baby)
-        rmap = dict(zip(plan.baby, rots))
+        lazy = self.cfg.lazy_moddown and hasattr(be, "rotate_hoisted_ext")
+        if lazy:
+            nz = [b for b in plan.baby if b % self.n]
+            ext = dict(zip(nz, be.rotate_hoisted_ext(ct, nz))) if nz else {}
+            if any(b % self.n == 0 for b in plan.baby):
+                ext.update({b: be.extend(ct) for b in plan.baby if b % self.n == 0})
+        else:
+            rmap = dict(zip(plan.baby, be.rotate_hoisted(ct, plan.baby)))
         groups = []
         for k in sorted(plan.giants, key=lambda k: (k != 0, k)):   # the unrotated giant first
             terms = plan.giants[k]
@@ -367,10 +386,10 @@ class Bootstrapper:
             for b in plan.baby:
                 bu = b // plan.unit
                 if bu in terms:
-                    pt = self._pt((tag, k, bu), terms[bu] * const, l, S_p)
-                    pairs.append((rmap[b], pt))
+                    pt = self._pt((tag, k, bu, lazy), terms[bu] * const, l, S_p, ext=lazy)
+                    pairs.append(((ext if lazy else rmap)[b], pt))
             groups.append(((k * plan.g * plan.unit) % self.n, pairs))
-        acc = be.bsgs_combine(groups)
+        acc = be.bsgs_combine_ext(groups) if lazy else be.bsgs_combine(groups)
         return be.rescale2(acc) if nres == 2 else be.rescale(acc)
 
     def _match(self, ct, level, scale):
@@ -547,6 +566,13 @@ class ListBatch:
         self.level, self.scale = self.cts[0].level, self.cts[0].scale
 
 
+class ExtCt:
+    """A ciphertext over the extended basis Q_l P (eval domain) before mod_down: data (2, ext, N)."""
+
+    def __init__(self, data, scale, level):
+        self.data, self.scale, self.level = data, Fraction(scale), level
+
+
 class CtBatch:
     """B ciphertexts at one level and scale in one (B, 2, level+1, N) device tensor; the GPU
     backend runs every operation on all of them in one batched launch."""
@@ -647,11 +673,117 @@ class GpuBackend:
         return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
                                  RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale, L)
 
-    def encode_slots(self, values, level, scale):
+    def encode_slots(self, values, level, scale, ext=False):
         from .encoding import Plaintext, signed_to_eval
-        from .poly import main_ids
+        from .poly import extended_ids, main_ids
         ints = encode_ints(values, self.params.N, scale)
+        if ext:                      # extended basis (main 0..level + specials): hoisted ModDown
+            pt = Plaintext.__new__(Plaintext)
+            pt.poly = signed_to_eval(ints, self.params, extended_ids(self.params, level))
+            pt.scale, pt.level, pt.compression = Fraction(scale), level, "ext"
+            return pt
         return Plaintext(signed_to_eval(ints, self.params, main_ids(level)), Fraction(scale), level)
+
+    # hoisted-ModDown BSGS (extended-basis ciphertexts: ExtCt with data (2, ext, N))
+    def extend(self, ct):
+        """P * ct over the extended basis (special rows zero): its mod_down is exactly ct."""
+        import torch
+        from .poly import LF_OP_SCALAR_MUL, ewise, main_ids
+        l1 = ct.level + 1
+        ext = l1 + self.params.num_special
+        data = torch.zeros((2, ext, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
+        P = self.params.special_product()
+        sc = [P % q for q in self.params.rns_basis[:l1]]
+        ewise(self.params, LF_OP_SCALAR_MUL, data[0, :l1], ct.b.limbs, main_ids(ct.level), scalars=sc)
+        ewise(self.params, LF_OP_SCALAR_MUL, data[1, :l1], ct.a.limbs, main_ids(ct.level), scalars=sc)
+        return ExtCt(data, ct.scale, ct.level)
+
+    def rotate_hoisted_ext(self, ct, steps):
+        import ctypes
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .fused import ct_block
+        ctx = get_context(self.params)
+        n = len(steps)
+        lib = _native.lib()
+        level = ct.level
+        ext = level + 1 + self.params.num_special
+        ws = torch.empty(lib.lf_rotate_hoisted_workspace_bytes(ctx.handle, level, n) // 4,
+                         dtype=torch.int32, device="cuda")
+        out = torch.empty((n, 2, ext, self.params.N), dtype=torch.int32, device="cuda")
+        gs = [galois_element_of(self.params.N, s) for s in steps]
+        keys = [self.rk[s % self.params.n] for s in steps]
+        karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
+        c = ct_block(ct)
+        _native.check(lib.lf_rotate_hoisted_ext(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
+                                                dptr(out), out[0].numel(), dptr(ws), stream_handle()),
+                      "lf_rotate_hoisted_ext")
+        return [ExtCt(out[i], ct.scale, level) for i in range(n)]
+
+    def bsgs_combine_ext(self, groups):
+        """Per giant step: sum_b ext_b * pt_{k,b} over the extended basis (lf_ptmac_rows) into one
+        batch, ONE batched mod_down of all giant steps (lf_moddown_ext), then the batched giant
+        rotations and the final sum (rotate_and_sum)."""
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .poly import Domain, RnsPolynomial, extended_ids, main_ids
+        ctx = get_context(self.params)
+        lib = _native.lib()
+        x0 = groups[0][1][0][0]
+        level = x0.level
+        ext_ids = extended_ids(self.params, level)
+        ext = len(ext_ids)
+        N = self.params.N
+        G = len(groups)
+        inner = torch.empty((G, 2, ext, N), dtype=torch.int32, device="cuda")
+        pidx = ctx.pidx_array(ext_ids)
+        for i, (_, pairs) in enumerate(groups):
+            assert len(pairs) <= 32
+            n = len(pairs)
+            bp = (ctypes_void_p * n)(*[x.data[0].data_ptr() for x, _ in pairs])
+            ap = (ctypes_void_p * n)(*[x.data[1].data_ptr() for x, _ in pairs])
+            pp = (ctypes_void_p * n)(*[pt.poly.limbs.data_ptr() for _, pt in pairs])
+            _native.check(lib.lf_ptmac_rows(ctx.handle, ctypes_void_p(inner[i].data_ptr()), ext, pidx, n,
+                                            bp, ap, pp, stream_handle()), "lf_ptmac_rows")
+        scale = x0.scale * groups[0][1][0][1].scale
+        out = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
+        ws = torch.empty(lib.lf_moddown_workspace_bytes(ctx.handle, level, G) // 4, dtype=torch.int32,
+                         device="cuda")
+        _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(out),
+                                         out[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
+        ids = main_ids(level)
+        cts = [self.C.Ciphertext(RnsPolynomial(out[i, 0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[i, 1], Domain.EVAL, ids), scale, level) for i in range(G)]
+        return self.rotate_and_sum([(st, c) for (st, _), c in zip(groups, cts)], batch=out)
+
+    def rotate_and_sum(self, items, batch=None):
+        """sum_k rot_{s_k}(ct_k): the rotated ones in one lf_rotate_batch pipeline (they must be
+        contiguous in `batch` when given), the sum in one linear-combination launch."""
+        import torch
+        from . import fused
+        from .poly import Domain, RnsPolynomial, main_ids
+        ct0 = items[0][1]
+        level, scale = ct0.level, ct0.scale
+        parts = [c for st, c in items if st % self.params.n == 0]
+        rot = [(i, st) for i, (st, _) in enumerate(items) if st % self.params.n]
+        if rot:
+            lo, hi = rot[0][0], rot[-1][0] + 1
+            assert [i for i, _ in rot] == list(range(lo, hi)), "rotated giants must be contiguous"
+            src = batch[lo:hi] if batch is not None else torch.stack(
+                [torch.stack([c.b.limbs, c.a.limbs]) for _, c in items[lo:hi]])
+            gs = [galois_element_of(self.params.N, st) for _, st in rot]
+            keys = [self.rk[st % self.params.n] for _, st in rot]
+            r = fused.rotate_batch(self.params, level, src, gs, keys)
+            ids = main_ids(level)
+            parts.extend(self.C.Ciphertext(RnsPolynomial(r[j, 0], Domain.EVAL, ids),
+                                           RnsPolynomial(r[j, 1], Domain.EVAL, ids), scale, level)
+                         for j in range(hi - lo))
+        if len(parts) == 1:
+            return parts[0]
+        acc = self.lincomb([(c, 1.0, Fraction(1)) for c in parts])
+        return self.C.Ciphertext(acc.b, acc.a, scale, level)
 
     # arithmetic
     def _b_ewise(self, op, x, y):

@@ -196,7 +196,20 @@ int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint3
   if (nrows < 1 || nrows > ctx->nprimes) { lf_set_error("lf_ptmac: bad nrows %d", nrows); return 2; }
   for (int i = 0; i < nterm; ++i)
     if (!b[i] || !a[i] || !pt[i]) { lf_set_error("lf_ptmac: null term %d", i); return 1; }
-  return lf_launch_ptmac(ctx, out, nrows, nterm, b, a, pt, (cudaStream_t)stream);
+  return lf_launch_ptmac(ctx, out, nrows, nterm, b, a, pt, nullptr, (cudaStream_t)stream);
+}
+
+int lf_ptmac_rows(const lf_ctx* ctx, uint32_t* out, int nrows, const int32_t* prime_idx, int nterm,
+                  const uint32_t* const* b, const uint32_t* const* a, const uint32_t* const* pt,
+                  void* stream) {
+  if (!ctx || !out || !b || !a || !pt || !prime_idx) { lf_set_error("lf_ptmac_rows: null argument"); return 1; }
+  if (nterm < 1 || nterm > LF_PTMAC_MAX) { lf_set_error("lf_ptmac_rows: nterm %d outside [1, %d]", nterm, LF_PTMAC_MAX); return 2; }
+  if (nrows < 1 || nrows > LF_MAX_ROWS) { lf_set_error("lf_ptmac_rows: bad nrows %d", nrows); return 2; }
+  for (int r = 0; r < nrows; ++r)
+    if (prime_idx[r] < 0 || prime_idx[r] >= ctx->nprimes) { lf_set_error("lf_ptmac_rows: bad prime index"); return 2; }
+  for (int i = 0; i < nterm; ++i)
+    if (!b[i] || !a[i] || !pt[i]) { lf_set_error("lf_ptmac_rows: null term %d", i); return 1; }
+  return lf_launch_ptmac(ctx, out, nrows, nterm, b, a, pt, prime_idx, (cudaStream_t)stream);
 }
 
 int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,

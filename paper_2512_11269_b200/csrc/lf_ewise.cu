@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(256) k_modraise(u32* out, const u32* in, int n
 struct PtMacArgs {
   u32* out;                 // 2 x nrows rows
   int nterm, nrows;
+  RowMap rm;                // prime index of each row
   const u32* b[LF_PTMAC_MAX];
   const u32* a[LF_PTMAC_MAX];
   const u32* pt[LF_PTMAC_MAX];
@@ -127,7 +128,7 @@ struct PtMacArgs {
 __global__ void __launch_bounds__(256) k_ptmac(PtMacArgs A, LfDev dv) {
   const int row = blockIdx.y;                   // 0 .. 2*nrows-1
   const int p = row / A.nrows, r = row % A.nrows;
-  const PrimeK k = dv.pk[r];
+  const PrimeK k = dv.pk[A.rm.p[r]];
   const size_t N = (size_t)1 << dv.logN;
   const size_t off = (size_t)r * N;
   for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < N / 4;
@@ -228,9 +229,11 @@ int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int n
 }
 
 int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
-                    const u32* const* a, const u32* const* pt, cudaStream_t s) {
+                    const u32* const* a, const u32* const* pt, const int32_t* pidx, cudaStream_t s) {
   PtMacArgs A;
   A.out = out; A.nterm = nterm; A.nrows = nrows;
+  A.rm.n = nrows;
+  for (int r = 0; r < nrows; ++r) A.rm.p[r] = (unsigned char)(pidx ? pidx[r] : r);
   for (int i = 0; i < nterm; ++i) { A.b[i] = b[i]; A.a[i] = a[i]; A.pt[i] = pt[i]; }
   const int nv = ctx->N / 4;
   const int bx = (nv + 255) / 256 < 16 ? (nv + 255) / 256 : 16;

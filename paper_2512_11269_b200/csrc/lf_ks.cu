@@ -340,6 +340,12 @@ struct KsInnerArgs {
   const u32* rowk;     // plan: per main row {s, s', pinv, pinv'}
   int level, d, beta, L, alpha, R;
   int nbatch;          // grid.x = batch (fastest, so a key line is reused from L2) x lines
+  int pre;             // 1: T1 holds finished eval-domain pieces (natural layout, k_pieces ran once
+                       //    for a hoisted batch): no row NTT here, only the permuted load + MAC
+  int ext_out;         // 1: write (P*sigma_g(b) + acc_b, acc_a) over the extended basis, eval domain,
+                       //    into acc (2 x ext rows per instance) and skip ModDown (hoisted-ModDown BSGS)
+  const u32* eb;       // ext_out: ct.b rows (shared by all instances), P mod q_t table
+  const u32* pmod;
   const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
   u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
 };
@@ -388,7 +394,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   auto prefetch_digit = [&](int j) {
     if (j >= A.beta) return;
     const size_t lo = ((size_t)hi << L2) + (size_t)tl * C::E;
-    if (j != own_j)
+    if (j != own_j || A.pre)
       prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
     prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
     prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
@@ -406,7 +412,20 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   for (int j = 0; j < A.beta; ++j) {
     prefetch_digit(j + 1);
     u32 pc[C::E];
-    if (j == own_j) {
+    if (A.pre) {
+      // finished piece: load the source line, permute inside it (sigma_g) through smem
+      load_row_step2<L2>(pc, A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2), tl);
+      if (GALOIS) {
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) {
+          const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+          pc[e] = perm_buf[auto_src_index(pos, gal, logN) & (M2 - 1)];
+        }
+      }
+    } else if (j == own_j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
       const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
       const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
@@ -454,7 +473,20 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   u32 rb[C::E], ra[C::E];
 #pragma unroll
   for (int e = 0; e < C::E; ++e) { rb[e] = reduce64(accb[e], pk); ra[e] = reduce64(acca[e], pk); }
-  if (is_main) {
+  if (A.ext_out) {
+    if (is_main) {      // + P * sigma_g(b): the b part of the rotation before the division by P
+      const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
+      const u32* br = A.eb + ((size_t)t << logN);
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) {
+        const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+        const u32 v = br[GALOIS ? auto_src_index(pos, gal, logN) : pos];
+        rb[e] = addmod(rb[e], mul_shoup(v, pm, pmp, pk.q), pk.q);
+      }
+    }
+    store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(ext + t) << logN) + ((size_t)hi << L2), tl);
+  } else if (is_main) {
     store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
     store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2), tl);
   } else {
@@ -754,7 +786,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
 // Materialised pieces (keyswitch_decompose API): finish the NTT of T1 rows, own rows x*s.
 template <int L1, int L2>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
-k_pieces(const u32* __restrict__ T1, const u32* __restrict__ x, u32* __restrict__ out,
+k_pieces(const u32* T1, const u32* __restrict__ x, u32* out,
          const u32* rowk, int level, int d, int L, int alpha, LfDev dv) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
@@ -909,6 +941,7 @@ struct KsCall {
   u32 g;                    // galois element (ROT): glist[b0+b] if given, else g
   const u32* glist;
   int b0;                   // first instance of this chunk
+  bool ext_out;             // stop after the inner product: out = 2 x ext rows per instance
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -953,6 +986,16 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.tsplit = bc_tsplit(K.beta, nsh, (1 << L2) / 8, mmax);
     if (int e = launch_bc_auto<L1, L2>(ctx, A, nsh, kmax, s)) return e;
   }
+  // hoisted batch: finish the NTT of every piece ONCE (in place, natural layout); each rotation's
+  // inner product then only permutes and multiplies (no per-rotation row NTT)
+  const bool pre = c.hoisted && c.batch > 1;
+  if (pre) {
+    dim3 grid(K.beta * K.ext * groups);
+    lf_smem_optin(k_pieces<L1, L2>, smR);
+    k_pieces<L1, L2><<<grid, S::TRR, smR, s>>>(w.T1, c.x, w.T1, P->rowk, c.level, P->d, P->L,
+                                              P->n_special, dv);
+    LF_CHECK_LAUNCH();
+  }
   LF_MARK(2);
   // K_C
   {
@@ -961,11 +1004,14 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.t1_bs = w.per_sh; A.x_bs = c.x_bs; A.acc_bs = w.per; A.t2_bs = w.per;
     A.rowk = P->rowk; A.level = c.level; A.d = P->d; A.beta = K.beta; A.L = P->L; A.alpha = alpha;
     A.R = P->L + 1 + alpha; A.nbatch = c.batch;
+    A.ext_out = c.ext_out ? 1 : 0;
+    A.pre = pre ? 1 : 0;
+    if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
 #ifndef LF_KSI_PF
 #define LF_KSI_PF 0
 #endif
-    if (LF_KSI_PF) {
+    if (LF_KSI_PF && !c.ext_out) {
     constexpr int LPK = S::LPCR >= 16 ? 8 : S::LPCR;        // lines per CTA (2 CTAs / SM)
     constexpr int NTK = KsiShape<L2, LPK>::NT;
     dim3 grid(K.ext * ((1 << L1) / LPK) * c.batch);
@@ -992,6 +1038,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     LF_CHECK_LAUNCH();
   }
   LF_MARK(3);
+  if (c.ext_out) return 0;
   // K_BC (ModDown)
   {
     BcArgs A{};
@@ -1067,6 +1114,53 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
     A.scal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)l * P->n_main * 2; A.sstride = 2;
     A.nt = nt; A.nacc = l + 1; A.ne = 0;
     dim3 grid(nt * groups, 1, batch);
+    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
+    LF_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+// ModDown of both polynomials of an extended-basis ciphertext (poly.py:251-281 twice): row
+// INTT of the 2 alpha special rows, BConv onto the main primes, row NTT + (x - conv) P^-1.
+template <int L1, int L2>
+static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t in_bs, u32* out,
+                            size_t out_bs, int batch, void* ws, cudaStream_t s) {
+  using S = NttShape<L1, L2>;
+  const LfKsPlan* P = ctx->ks;
+  const int l1 = level + 1, alpha = P->n_special, ext = l1 + alpha;
+  const size_t N = ctx->N;
+  const LfDev dv = ctx->dev();
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
+  const int groups = (1 << L1) / S::LPCR;
+  u32* T2 = (u32*)ws;                              // per instance: 2 alpha rows, then T3: 2 (l+1)
+  const size_t per = (2 * (size_t)alpha + 2 * (size_t)l1) * N;
+  u32* T3 = T2 + 2 * (size_t)alpha * N;
+  {
+    dim3 grid(2 * alpha * groups, 1, batch);
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1); }
+    LF_CHECK_LAUNCH();
+  }
+  {
+    BcArgs A{};
+    A.src = T2; A.dst = T3; A.src_bs = per; A.dst_bs = per;
+    A.ngroups = 2;
+    for (int p = 0; p < 2; ++p) {
+      A.g[p].B = P->down;
+      A.g[p].B.m = l1;
+      A.g[p].src_rows = P->iota;
+      A.g[p].dst_rows = P->iota;
+      A.g[p].src_row0 = p * alpha;
+      A.g[p].dst_row0 = p * l1;
+    }
+    A.tsplit = bc_tsplit(2, batch, (1 << L2) / 8, l1);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, batch, alpha, s)) return e;
+  }
+  {
+    ModDownArgs A{};
+    A.T3 = T3; A.acc = in; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
+    A.t3_bs = per; A.acc_bs = in_bs; A.out_bs = out_bs; A.e_bs = 0;
+    A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = ext; A.ne = 0;
+    dim3 grid(l1 * groups, 1, batch);
     { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
     LF_CHECK_LAUNCH();
   }
@@ -1291,6 +1385,41 @@ int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct
 #define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ndrop, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
   LF_DISPATCH_LOGN(ctx->logN, LF_RS)
 #undef LF_RS
+  return 0;
+}
+
+int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                          const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                          size_t out_bstride, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct || !gs || !keys || !out_ext || !workspace || n_rot < 1) {
+    lf_set_error("lf_rotate_hoisted_ext: bad argument");
+    return 1;
+  }
+  for (int r = 0; r < n_rot; ++r)
+    if (!(gs[r] & 1) || !keys[r]) { lf_set_error("lf_rotate_hoisted_ext: rotation %d: bad key or even galois element", r); return 2; }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = n_rot; c.op = OP_ROT; c.hoisted = true; c.ext_out = true;
+  c.x = ct + arow; c.x2 = c.x; c.x_bs = 0; c.keylist = keys;
+  c.out = out_ext; c.out_bs = out_bstride; c.e0 = ct; c.e1 = nullptr; c.e_bs = 0;
+  c.glist = gs;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
+  if (ks_check(ctx, level)) return 0;
+  return (2 * (size_t)ctx->ks->n_special + 2 * (size_t)(level + 1)) * ctx->N * 4 *
+         (size_t)(batch < 1 ? 1 : batch);
+}
+
+int lf_moddown_ext(const lf_ctx* ctx, int level, const uint32_t* in_ext, size_t in_bstride,
+                   uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!in_ext || !out || !workspace || batch < 1) { lf_set_error("lf_moddown_ext: bad argument"); return 1; }
+#define LF_MD(A, B) { if (int e = moddown_pipeline<A, B>(ctx, level, in_ext, in_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_MD)
+#undef LF_MD
   return 0;
 }
 

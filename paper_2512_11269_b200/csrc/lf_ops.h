@@ -14,7 +14,7 @@ int lf_launch_bconv(const LfCtx* ctx, u32* out, const u32* src, const u32* tab, 
 int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
                        cudaStream_t s);
 int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
-                    const u32* const* a, const u32* const* pt, cudaStream_t s);
+                    const u32* const* a, const u32* const* pt, const int32_t* pidx, cudaStream_t s);
 #define LF_LINCOMB_MAX 8
 #define LF_LINCOMB_ROWS 64
 int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,

@@ -139,7 +139,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
       if (t % d != j) f = mulm(f, primes[t] % q, q);
     return invm(f, q);
   };
-  std::vector<u32> rowk;
+  std::vector<u32> rowk, pmodv;
   for (int t = 0; t <= L; ++t) {
     const u32 q = primes[t];
     const u32 s = dec_scalar(t % d, t);
@@ -147,8 +147,10 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
     for (int j = 0; j < n_sp; ++j) P = mulm(P, primes[n_main + j] % q, q);
     const u32 pinv = invm(P, q);
     rowk.insert(rowk.end(), {s, shoupc(s, q), pinv, shoupc(pinv, q)});
+    pmodv.insert(pmodv.end(), {P, shoupc(P, q)});
   }
   const size_t off_rowk = blob.push(rowk);
+  const size_t off_pmod = blob.push(pmodv);
   std::vector<u32> qinv((size_t)n_main * n_main * 2, 0);
   for (int l = 1; l <= L; ++l)
     for (int t = 0; t < l; ++t) {
@@ -235,6 +237,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
   P->dmem = dmem;
   P->iota = (const int*)(base + off_iota);
   P->rowk = base + off_rowk;
+  P->pmod = base + off_pmod;
   P->qinv = base + off_qinv;
   P->qinv2 = base + off_qinv2;
   P->down = view(down);

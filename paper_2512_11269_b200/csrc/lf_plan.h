@@ -31,6 +31,7 @@ struct LfKsPlan {
   BconvDev down;                   // ModDown: specials -> main 0..L (prefix per level)
   const int* iota;                 // device 0..max(n_main, n_special) identity row list
   const u32* rowk;                 // [n_main][4]: s_t, s_t' (own-digit decomposition scalar), P^-1, P^-1'
+  const u32* pmod;                 // [n_main][2]: P mod q_t and Shoup companion (extended rotations)
   const u32* qinv;                 // [n_main][n_main][2]: q_l^-1 mod q_t and Shoup companion
   const u32* qinv2;                // [n_main][n_main][2]: (q_l q_{l-1})^-1 mod q_t, companion
   void* dmem;
