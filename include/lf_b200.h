@@ -199,6 +199,12 @@ int lf_ptmac_rows(const lf_ctx* ctx, uint32_t* out, int nrows, const int32_t* pr
                   const uint32_t* const* b, const uint32_t* const* a, const uint32_t* const* pt,
                   void* stream);
 
+/* mul_plain by a compressed plaintext (reference compress.py:163-176): unique holds nrows x
+ * unique_count values (eval domain); position i of row r reads unique[r][i / (N/unique_count)].
+ * ct / out: 2 x nrows rows (b then a).  Bit-equal to mul_plain with the expanded plaintext. */
+int lf_mul_compressed(const lf_ctx* ctx, uint32_t* out, const uint32_t* ct, const uint32_t* unique,
+                      int nrows, int unique_count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

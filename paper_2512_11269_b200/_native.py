@@ -78,6 +78,8 @@ def _load():
         "lf_ptmac_rows": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, _i32_host, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                                          ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
+        "lf_mul_compressed": (ctypes.c_int, [ctypes.c_void_p, _u32p, _u32p, _u32p, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_void_p]),
         "lf_ks_decompose": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, _u32p, ctypes.c_void_p,
                                            ctypes.c_void_p]),
         "lf_modraise": (ctypes.c_int, [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_int,

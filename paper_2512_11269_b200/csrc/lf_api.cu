@@ -232,4 +232,17 @@ int lf_rows_to_u64(uint64_t* out, const uint32_t* in, size_t n, void* stream) {
   return lf_launch_convert(out, in, n, false, (cudaStream_t)stream);
 }
 
+int lf_mul_compressed(const lf_ctx* ctx, uint32_t* out, const uint32_t* ct, const uint32_t* unique,
+                      int nrows, int unique_count, void* stream) {
+  if (!ctx || !out || !ct || !unique) { lf_set_error("lf_mul_compressed: null argument"); return 1; }
+  if (nrows < 1 || nrows > ctx->nprimes) { lf_set_error("lf_mul_compressed: bad nrows %d", nrows); return 2; }
+  if (unique_count < 1 || unique_count > ctx->N || (unique_count & (unique_count - 1)) || ctx->N % unique_count) {
+    lf_set_error("lf_mul_compressed: unique_count %d must be a power of two dividing N", unique_count);
+    return 2;
+  }
+  int lb = 0;
+  while ((unique_count << lb) < ctx->N) ++lb;
+  return lf_launch_mul_compressed(ctx, out, ct, unique, nrows, unique_count, lb, (cudaStream_t)stream);
+}
+
 }  // extern "C"

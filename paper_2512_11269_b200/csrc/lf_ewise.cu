@@ -218,6 +218,32 @@ int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStre
   return 0;
 }
 
+// Compressed-plaintext multiply (reference compress.py:163-176): the plaintext row stores one
+// value per block of `1 << lb` consecutive evaluation positions; out = ct * unique[pos >> lb].
+__global__ void __launch_bounds__(256) k_mul_compressed(u32* out, const u32* ct, const u32* uq,
+                                                        int nrows, int ucount, int lb, LfDev dv) {
+  const size_t N = (size_t)1 << dv.logN;
+  const size_t total = N * 2 * nrows;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t rr = idx >> dv.logN;           // p * nrows + row
+    const int row = (int)(rr % nrows);
+    const u32 pos = (u32)(idx & (N - 1));
+    const PrimeK k = dv.pk[row];
+    out[idx] = mulmod(ct[idx], uq[(size_t)row * ucount + (pos >> lb)], k);
+  }
+}
+
+int lf_launch_mul_compressed(const LfCtx* ctx, u32* out, const u32* ct, const u32* uq, int nrows,
+                             int ucount, int lb, cudaStream_t s) {
+  const size_t total = (size_t)ctx->N * 2 * nrows;
+  size_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_mul_compressed<<<(unsigned)blocks, 256, 0, s>>>(out, ct, uq, nrows, ucount, lb, ctx->dev());
+  LF_CHECK_LAUNCH();
+  return 0;
+}
+
 int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int nout,
                        cudaStream_t s) {
   const size_t total = (size_t)ctx->N * nin * nout;

@@ -33,3 +33,6 @@ LevelMismatch = _mk("LevelMismatch")
 ScaleMismatch = _mk("ScaleMismatch")
 LevelExhausted = _mk("LevelExhausted")
 MissingRotationKey = _mk("MissingRotationKey")
+BadStride = _mk("BadStride", doc="Compression stride is not a power of two dividing n.")
+NotPeriodic = _mk("NotPeriodic", doc="Slot vector is not exactly periodic with the stride.")
+BaseMismatch = _mk("BaseMismatch", doc="Compressed plaintext has no limb for the requested base.")
