@@ -918,9 +918,12 @@ static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax
 }
 
 static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax) {
-  // expose enough CTAs to fill 148 SMs a few times over; each split redoes the INTT prologue
+  // Split the target range over a cluster only while the launch has fewer CTAs than ~2/3 of
+  // the 148 SMs: each CTA then converts all its targets from one source tile (no DSMEM
+  // exchange), which measured fastest whenever the grid already covers the GPU (C2 batch 1:
+  // ModUp 75 -> 63 us unsplit; ModDown with 2 groups needs the split: 64 -> 43 us).
   int ts = 1;
-  while (ts < 8 && (long)ngroups * batch * ncoltiles * ts < 148 * 4 && mmax / (ts * 2) >= 6) ts *= 2;
+  while (ts < 8 && (long)ngroups * batch * ncoltiles * ts < 96 && mmax / (ts * 2) >= 4) ts *= 2;
   return ts;
 }
 
