@@ -5,6 +5,15 @@
 #include "lf_bconv.cuh"
 #include "lf_ops.h"
 
+#define LF_LAUNCH_CHECK_EW(call)                                               \
+  do {                                                                         \
+    cudaError_t e__ = (call);                                                  \
+    if (e__ != cudaSuccess) {                                                  \
+      lf_set_error("%s:%d: launch: %s", __FILE__, __LINE__, cudaGetErrorString(e__)); \
+      return 3;                                                                \
+    }                                                                          \
+  } while (0)
+
 struct EwArgs {
   u32* out;
   const u32* a;
@@ -33,6 +42,8 @@ LF_DEV u32 ew_one(int op, u32 a, u32 b, u32 c, u32 s, u32 sp, const PrimeK& k) {
 }
 
 __global__ void __launch_bounds__(256) k_ewise(EwArgs A, LfDev dv, int logN) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const int row = blockIdx.y;
   const PrimeK k = dv.pk[A.rm.p[row]];
   const u32 s = A.s[row], sp = A.sp[row];
@@ -60,6 +71,8 @@ __global__ void __launch_bounds__(256) k_ewise(EwArgs A, LfDev dv, int logN) {
 // out[r][i] = in[r][perm_g(i)]   (out must not alias in)
 __global__ void __launch_bounds__(256) k_automorph(u32* out, const u32* in, u32 g, int logN,
                                                    int nrows) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const size_t N = (size_t)1 << logN;
   const size_t total = N * nrows;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
@@ -72,6 +85,8 @@ __global__ void __launch_bounds__(256) k_automorph(u32* out, const u32* in, u32 
 
 // Coefficient-domain exact conversion: src (k rows) -> out (m rows), one thread per coeff.
 __global__ void __launch_bounds__(128) k_bconv(u32* out, const u32* src, BconvDev B, LfDev dv) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const size_t N = (size_t)1 << dv.logN;
   const size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -93,6 +108,8 @@ __global__ void __launch_bounds__(128) k_bconv(u32* out, const u32* src, BconvDe
 // the primes of nout rows: out[i*nout + r] = lift(in[i]) mod q_r.
 __global__ void __launch_bounds__(256) k_modraise(u32* out, const u32* in, int nin, int nout,
                                                   LfDev dv) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const size_t N = (size_t)1 << dv.logN;
   const u32 q0 = dv.pk[0].q;
   const size_t total = N * nin * nout;
@@ -126,6 +143,8 @@ struct PtMacArgs {
 };
 
 __global__ void __launch_bounds__(256) k_ptmac(PtMacArgs A, LfDev dv) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const int row = blockIdx.y;                   // 0 .. 2*nrows-1
   const int p = row / A.nrows, r = row % A.nrows;
   const PrimeK k = dv.pk[A.rm.p[r]];
@@ -159,6 +178,8 @@ struct LinCombArgs {
 };
 
 __global__ void __launch_bounds__(256) k_lincomb(LinCombArgs A, LfDev dv) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const int row = blockIdx.y;
   const int p = row / A.nrows, r = row % A.nrows;
   const PrimeK k = dv.pk[r];
@@ -192,7 +213,7 @@ int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u3
   const int nv = ctx->N / 4;
   const int bx = (nv + 255) / 256 < 16 ? (nv + 255) / 256 : 16;
   dim3 grid(bx, 2 * nrows);
-  k_lincomb<<<grid, 256, 0, s>>>(A, ctx->dev());
+  LF_LAUNCH_CHECK_EW(lf_launch(k_lincomb, dim3(grid), dim3(256), 0, s, 1, A, ctx->dev()));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -200,10 +221,14 @@ int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u3
 // Wire-format conversion (LFHE rows are little-endian uint64, serial.py:1-14): narrow to the
 // device's uint32 residues (values < 2^28) or widen back.
 __global__ void __launch_bounds__(256) k_narrow(u32* out, const unsigned long long* in, size_t n) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = (u32)in[i];
 }
 __global__ void __launch_bounds__(256) k_widen(unsigned long long* out, const u32* in, size_t n) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = in[i];
 }
@@ -212,8 +237,8 @@ int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStre
   size_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks == 0) return 0;
-  if (narrow) k_narrow<<<(unsigned)blocks, 256, 0, s>>>((u32*)out, (const unsigned long long*)in, n);
-  else k_widen<<<(unsigned)blocks, 256, 0, s>>>((unsigned long long*)out, (const u32*)in, n);
+  if (narrow) LF_LAUNCH_CHECK_EW(lf_launch(k_narrow, dim3((unsigned)blocks), dim3(256), 0, s, 1, (u32*)out, (const unsigned long long*)in, n));
+  else LF_LAUNCH_CHECK_EW(lf_launch(k_widen, dim3((unsigned)blocks), dim3(256), 0, s, 1, (unsigned long long*)out, (const u32*)in, n));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -222,6 +247,8 @@ int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStre
 // value per block of `1 << lb` consecutive evaluation positions; out = ct * unique[pos >> lb].
 __global__ void __launch_bounds__(256) k_mul_compressed(u32* out, const u32* ct, const u32* uq,
                                                         int nrows, int ucount, int lb, LfDev dv) {
+  lf_pdl_trigger();
+  lf_pdl_wait();
   const size_t N = (size_t)1 << dv.logN;
   const size_t total = N * 2 * nrows;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
@@ -239,7 +266,7 @@ int lf_launch_mul_compressed(const LfCtx* ctx, u32* out, const u32* ct, const u3
   const size_t total = (size_t)ctx->N * 2 * nrows;
   size_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_mul_compressed<<<(unsigned)blocks, 256, 0, s>>>(out, ct, uq, nrows, ucount, lb, ctx->dev());
+  LF_LAUNCH_CHECK_EW(lf_launch(k_mul_compressed, dim3((unsigned)blocks), dim3(256), 0, s, 1, out, ct, uq, nrows, ucount, lb, ctx->dev()));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -249,7 +276,7 @@ int lf_launch_modraise(const LfCtx* ctx, u32* out, const u32* in, int nin, int n
   const size_t total = (size_t)ctx->N * nin * nout;
   size_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_modraise<<<(unsigned)blocks, 256, 0, s>>>(out, in, nin, nout, ctx->dev());
+  LF_LAUNCH_CHECK_EW(lf_launch(k_modraise, dim3((unsigned)blocks), dim3(256), 0, s, 1, out, in, nin, nout, ctx->dev()));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -264,7 +291,7 @@ int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32*
   const int nv = ctx->N / 4;
   const int bx = (nv + 255) / 256 < 16 ? (nv + 255) / 256 : 16;
   dim3 grid(bx, 2 * nrows);
-  k_ptmac<<<grid, 256, 0, s>>>(A, ctx->dev());
+  LF_LAUNCH_CHECK_EW(lf_launch(k_ptmac, dim3(grid), dim3(256), 0, s, 1, A, ctx->dev()));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -282,7 +309,7 @@ int lf_launch_ewise(const LfCtx* ctx, int op, u32* out, const u32* a, const u32*
   const int nv = ctx->N / 4;
   const int bx = (nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64;
   dim3 grid(bx, rm.n);
-  k_ewise<<<grid, 256, 0, s>>>(A, ctx->dev(), ctx->logN);
+  LF_LAUNCH_CHECK_EW(lf_launch(k_ewise, dim3(grid), dim3(256), 0, s, 1, A, ctx->dev(), ctx->logN));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -292,7 +319,7 @@ int lf_launch_automorph(const LfCtx* ctx, u32* out, const u32* in, u32 g, int nr
   const size_t total = (size_t)ctx->N * nrows;
   size_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_automorph<<<(unsigned)blocks, 256, 0, s>>>(out, in, g, ctx->logN, nrows);
+  LF_LAUNCH_CHECK_EW(lf_launch(k_automorph, dim3((unsigned)blocks), dim3(256), 0, s, 1, out, in, g, ctx->logN, nrows));
   LF_CHECK_LAUNCH();
   return 0;
 }
@@ -305,7 +332,7 @@ int lf_launch_bconv(const LfCtx* ctx, u32* out, const u32* src, const u32* tab, 
   }
   const BconvDev B = lf_bconv_view(tab, k, m, W);
   const int blocks = (ctx->N + 127) / 128;
-  k_bconv<<<blocks, 128, 0, s>>>(out, src, B, ctx->dev());
+  LF_LAUNCH_CHECK_EW(lf_launch(k_bconv, dim3(blocks), dim3(128), 0, s, 1, out, src, B, ctx->dev()));
   LF_CHECK_LAUNCH();
   return 0;
 }

@@ -26,6 +26,14 @@
 #include "lf_ops.h"
 
 #define LF_BC_MAXG 16
+#define LF_LAUNCH_CHECK(call)                                                  \
+  do {                                                                         \
+    cudaError_t e__ = (call);                                                  \
+    if (e__ != cudaSuccess) {                                                  \
+      lf_set_error("%s:%d: launch: %s", __FILE__, __LINE__, cudaGetErrorString(e__)); \
+      return 3;                                                                \
+    }                                                                          \
+  } while (0)
 #define LF_MAXB 64     // batch instances per launch (per-instance key / galois element)
 
 // Bulk L2 prefetch (TMA engine, sm_90+): warms the next stage's contiguous row segment so the
@@ -61,8 +69,10 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   const int pi = pbase + row % rpp;
   const PrimeK pk = dv.pk[pi];
   uint2* tws = reinterpret_cast<uint2*>(sm);
+  lf_pdl_trigger();
   stage_tree_async<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR,
                        threadIdx.x, blockDim.x);
+  lf_pdl_wait();
   const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) +
                      ((size_t)hi << L2);
   u32 v[C::E];
@@ -225,7 +235,9 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 
   const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
+  lf_pdl_trigger();
   for (int w = threadIdx.x; w < (t1 - t0) * k; w += blockDim.x) Wsm[w] = __ldg(&B.w[(size_t)t0 * k + w]);
+  lf_pdl_wait();
 
   // phase 1: INTT column pass of each source row, sources split over the groups and (when the
   // target range is split over a cluster) over the cluster's CTAs; the other CTAs' converted
@@ -399,9 +411,11 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
     prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
   };
-  prefetch_digit(0);
+  lf_pdl_trigger();
   stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
                        threadIdx.x, blockDim.x);
+  lf_pdl_wait();
+  prefetch_digit(0);
   cp_async_wait_all();
   __syncthreads();
 
@@ -614,8 +628,10 @@ k_ks_inner_pf(KsInnerArgs A, LfDev dv) {
     cp_async_commit();
   };
 
+  lf_pdl_trigger();
   stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, LPK, tid, NT);
   cp_async_commit();
+  lf_pdl_wait();
   issue(0);
   u64 accb[E], acca[E];
 #pragma unroll
@@ -721,7 +737,9 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   const u32 sc = A.scal[t * A.sstride], scp = A.scal[t * A.sstride + 1];
   uint2* tws = reinterpret_cast<uint2*>(sm);
   const u32 R0 = (1u << L1) + (blockIdx.x % groups) * S::LPCR;
+  lf_pdl_trigger();
   stage_tree_async<L2>(tws, dv.twf + ((size_t)t << logN), R0, S::LPCR, threadIdx.x, blockDim.x);
+  lf_pdl_wait();
   const TwTree tw{tws, R0, S::LPCR};
   u32* xs = rowpass_xs<L1, L2>(sm);
   const AddrR<L2> addr{ln * pitchR<L2>()};
@@ -802,6 +820,8 @@ k_pieces(const u32* T1, const u32* __restrict__ x, u32* out,
   const int pi = is_main ? t : L + 1 + (t - level - 1);
   const PrimeK pk = dv.pk[pi];
   const size_t lo0 = (size_t)hi << L2;
+  lf_pdl_trigger();
+  lf_pdl_wait();
   u32 v[C::E];
   if (is_main && t % d == j) {
     load_row_step2<L2>(v, x + ((size_t)t << logN) + lo0, tl);
@@ -868,26 +888,9 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
   auto kern = k_bconv_colpass<L1, L2, CW, KMAX, TG, KEX>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const long nblocks = (long)batch * ((1 << L2) / CW) * A.ngroups * A.tsplit;
-  if (A.tsplit > 1) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)nblocks);
-    cfg.blockDim = dim3(TG * CW * LineCfg<L1>::T);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = A.tsplit;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    LfDev dv = ctx->dev();
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, dv, kmax, batch);
-    if (e != cudaSuccess) { lf_set_error("bconv cluster launch: %s", cudaGetErrorString(e)); return 3; }
-  } else {
-    kern<<<(unsigned)nblocks, TG * CW * LineCfg<L1>::T, sm, s>>>(A, ctx->dev(), kmax, batch);
-  }
-  LF_CHECK_LAUNCH();
+  LfDev dv = ctx->dev();
+  LF_LAUNCH_CHECK(lf_launch(kern, dim3((unsigned)nblocks), dim3(TG * CW * LineCfg<L1>::T), sm, s,
+                            A.tsplit, A, dv, kmax, batch));
   return 0;
 }
 
@@ -969,9 +972,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   {
     dim3 grid(l1 * groups, 1, nsh);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); k_modup_in<L1, L2, 1><<<grid, S::TRR, smR, s>>>(c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0)); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -995,8 +998,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   if (pre) {
     dim3 grid(K.beta * K.ext * groups);
     lf_smem_optin(k_pieces<L1, L2>, smR);
-    k_pieces<L1, L2><<<grid, S::TRR, smR, s>>>(w.T1, c.x, w.T1, P->rowk, c.level, P->d, P->L,
-                                              P->n_special, dv);
+    LF_LAUNCH_CHECK(lf_launch(k_pieces<L1, L2>, dim3(grid), dim3(S::TRR), smR, s, 1, w.T1, c.x, w.T1, P->rowk, c.level, P->d, P->L,
+                                              P->n_special, dv));
     LF_CHECK_LAUNCH();
   }
   LF_MARK(2);
@@ -1021,22 +1024,22 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     if (c.op == OP_ROT) {
       const size_t smK = KsiShape<L2, LPK>::template bytes<3>();
       lf_smem_optin(k_ks_inner_pf<L1, L2, true, 0, LPK>, smK);
-      k_ks_inner_pf<L1, L2, true, 0, LPK><<<grid, NTK, smK, s>>>(A, dv);
+      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, true, 0, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
     } else if (c.op == OP_MUL) {
       const size_t smK = KsiShape<L2, LPK>::template bytes<4>();
       lf_smem_optin(k_ks_inner_pf<L1, L2, false, 1, LPK>, smK);
-      k_ks_inner_pf<L1, L2, false, 1, LPK><<<grid, NTK, smK, s>>>(A, dv);
+      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, false, 1, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
     } else {
       const size_t smK = KsiShape<L2, LPK>::template bytes<3>();
       lf_smem_optin(k_ks_inner_pf<L1, L2, false, 0, LPK>, smK);
-      k_ks_inner_pf<L1, L2, false, 0, LPK><<<grid, NTK, smK, s>>>(A, dv);
+      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, false, 0, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
     }
     } else {
     const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
     dim3 grid(K.ext * groups * c.batch);
-    if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); k_ks_inner<L1, L2, true, 0><<<grid, S::TRR, smC, s>>>(A, dv); }
-    else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, false, 1>, smC); k_ks_inner<L1, L2, false, 1><<<grid, S::TRR, smC, s>>>(A, dv); }
-    else { lf_smem_optin(k_ks_inner<L1, L2, false, 0>, smC); k_ks_inner<L1, L2, false, 0><<<grid, S::TRR, smC, s>>>(A, dv); }
+    if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, true, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, false, 1>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 1>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    else { lf_smem_optin(k_ks_inner<L1, L2, false, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
     }
     LF_CHECK_LAUNCH();
   }
@@ -1067,9 +1070,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1;
     for (int b = 0; b < c.batch; ++b) A.gs[b] = c.g_of(b);
     dim3 grid(l1 * groups, 1, c.batch);
-    if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); k_moddown_out<L1, L2, EPI_MUL><<<grid, S::TRR, smR, s>>>(A, dv); }
-    else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); k_moddown_out<L1, L2, EPI_ROT><<<grid, S::TRR, smR, s>>>(A, dv); }
-    else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
+    if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_MUL>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
+    else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_ROT>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
+    else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(5);
@@ -1098,7 +1101,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1117,7 +1120,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
     A.scal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)l * P->n_main * 2; A.sstride = 2;
     A.nt = nt; A.nacc = l + 1; A.ne = 0;
     dim3 grid(nt * groups, 1, batch);
-    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
+    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
   }
   return 0;
@@ -1140,7 +1143,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
   u32* T3 = T2 + 2 * (size_t)alpha * N;
   {
     dim3 grid(2 * alpha * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1164,7 +1167,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
     A.t3_bs = per; A.acc_bs = in_bs; A.out_bs = out_bs; A.e_bs = 0;
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = ext; A.ne = 0;
     dim3 grid(l1 * groups, 1, batch);
-    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); k_moddown_out<L1, L2, EPI_KS><<<grid, S::TRR, smR, s>>>(A, dv); }
+    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
   }
   return 0;
@@ -1183,7 +1186,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); k_modup_in<L1, L2, 0><<<grid, S::TRR, smR, s>>>(x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1201,8 +1204,8 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   {
     dim3 grid(K.beta * K.ext * groups);
     lf_smem_optin(k_pieces<L1, L2>, smR);
-    k_pieces<L1, L2><<<grid, S::TRR, smR, s>>>(w.T1, x, pieces, P->rowk, level, P->d, P->L,
-                                              P->n_special, dv);
+    LF_LAUNCH_CHECK(lf_launch(k_pieces<L1, L2>, dim3(grid), dim3(S::TRR), smR, s, 1, w.T1, x, pieces, P->rowk, level, P->d, P->L,
+                                              P->n_special, dv));
     LF_CHECK_LAUNCH();
   }
   return 0;
