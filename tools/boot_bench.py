@@ -15,7 +15,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 t0 = time.time()
 p = B.gen_params(65536, L, d=4, seed=0, scale=2 ** 26)
 sk, pk, rlk = B.keygen(p, seed=11)
-cfg = BT.BootConfig()
+cfg = BT.BootConfig(**{k: int(v) for k, v in (a.split("=") for a in sys.argv[3:] if "=" in a)})
+print("config", cfg)
 planner = BT.Bootstrapper(type("P", (), {"N": p.N, "main_primes": p.rns_basis}), cfg)
 rots = planner.required_rotations()
 ck, rk = BT.make_bootstrap_keys(p, sk, rots, seed=99)
