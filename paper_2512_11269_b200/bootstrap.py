@@ -40,10 +40,10 @@ Precision: see `DESIGN.md` §6 and `bench.py --workload bootstrap` (reported in 
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from fractions import Fraction
 from functools import lru_cache
-from math import ceil, pi
+from math import pi
 
 import numpy as np
 

@@ -36,13 +36,8 @@
   } while (0)
 #define LF_MAXB 64     // batch instances per launch (per-instance key / galois element)
 
-// Bulk L2 prefetch (TMA engine, sm_90+): warms the next stage's contiguous row segment so the
-// per-thread loads that follow hit L2 instead of HBM.  bytes must be a multiple of 16.
 LF_DEV void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-LF_DEV void prefetch_l2(const void* p, u32 bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 struct BcArgs {
@@ -515,196 +510,6 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   }
 }
 
-// K_C with a two-stage cp.async pipeline: every thread copies the next digit's key rows (b, a)
-// and piece (or own x) words straight into a private shared-memory slot while it computes the
-// current digit, so the global-load latency overlaps the row NTT.  Slots are laid out
-// chunk-major (word w of thread tid at ((w/4)*NT + tid)*4 + w%4) so every read is a
-// conflict-free LDS.128; no CTA barrier is needed because a thread only reads what it copied.
-LF_DEV void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
-}
-LF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-LF_DEV void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int L2, int LPK>
-struct KsiShape {
-  using C = LineCfg<L2>;
-  static constexpr int NT = LPK * C::T;
-  static constexpr int TW = ((2 * LPK * (C::M - 1) + 2) + 3) / 4 * 4;      // twiddle words
-  static constexpr int XW = LPK * (pitchR<L2>() + C::M);                  // exchange + perm words
-  static constexpr int EP = (C::E + 3) / 4 * 4;                            // padded words/slot
-  template <int NSLOT>
-  static constexpr size_t bytes() { return ((size_t)TW + XW + 2 * NSLOT * EP * NT) * 4; }
-};
-
-template <int E, int NT>
-LF_DEV int slot_idx(int w, int tid) { return ((w >> 2) * NT + tid) * 4 + (w & 3); }
-
-template <int E, int NT>
-LF_DEV void slot_read(u32* v, const u32* slot, int tid) {
-#pragma unroll
-  for (int c = 0; c < (E + 3) / 4; ++c) {
-    const uint4 q = *reinterpret_cast<const uint4*>(slot + (c * NT + tid) * 4);
-    if (4 * c + 0 < E) v[4 * c + 0] = q.x;
-    if (4 * c + 1 < E) v[4 * c + 1] = q.y;
-    if (4 * c + 2 < E) v[4 * c + 2] = q.z;
-    if (4 * c + 3 < E) v[4 * c + 3] = q.w;
-  }
-}
-
-// contiguous E words (step-2 layout of one line) -> slot
-template <int E, int NT>
-LF_DEV void slot_fill_contig(u32* slot, const u32* __restrict__ src, int tid) {
-  if constexpr (E % 4 == 0) {
-#pragma unroll
-    for (int c = 0; c < E / 4; ++c) cp_async16(slot + (c * NT + tid) * 4, src + 4 * c);
-  } else {
-#pragma unroll
-    for (int w = 0; w < E; ++w) cp_async4(slot + slot_idx<E, NT>(w, tid), src + w);
-  }
-}
-
-template <int L1, int L2, bool GALOIS, int XMODE, int LPK>
-__global__ void __launch_bounds__(LPK * LineCfg<L2>::T, 2)
-k_ks_inner_pf(KsInnerArgs A, LfDev dv) {
-  using C = LineCfg<L2>;
-  using K = KsiShape<L2, LPK>;
-  constexpr int E = C::E, T = C::T, M2 = C::M, NT = K::NT, EP = K::EP;
-  constexpr int logN = L1 + L2;
-  constexpr int BIN = NttShape<L1, L2>::FWD_C_OUT;
-  constexpr int NSLOT = XMODE == 1 ? 4 : 3;            // key b, key a, piece / x, x2
-  extern __shared__ __align__(16) u32 sm[];
-  const int tid = threadIdx.x, tl = tid % T, ln = tid / T;
-  constexpr int groups = (1 << L1) / LPK;
-  const size_t b = blockIdx.x % A.nbatch;
-  const int bl = blockIdx.x / A.nbatch;
-  const int t = bl / groups;                                 // ext position
-  const int hi0 = (bl % groups) * LPK, hi = hi0 + ln;
-  const int l = A.level;
-  const bool is_main = t <= l;
-  const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index == key row
-  const PrimeK pk = dv.pk[pi];
-  const int ext = l + 1 + A.alpha;
-  uint2* tws = reinterpret_cast<uint2*>(sm);
-  u32* xs = sm + K::TW + ln * (pitchR<L2>() + M2);
-  u32* perm_buf = xs + pitchR<L2>();
-  u32* stg = sm + K::TW + K::XW;
-  const AddrR<L2> addr{0};
-  const u32 gal = A.gs[b];
-  const u32* keyb = A.keyp[b];
-  int hs = hi, hi0s = hi0;
-  if (GALOIS) {
-    hs = (int)(auto_src_index((u32)hi << L2, gal, logN) >> L2);
-    hi0s = (int)((auto_src_index((u32)hi0 << L2, gal, logN) >> L2) / LPK) * LPK;
-  }
-  const int own_j = is_main ? t % A.d : -1;
-  const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
-  const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)t << logN);
-
-  auto issue = [&](int j) {
-    u32* st = stg + (j & 1) * (NSLOT * EP * NT);
-    const size_t lo = ((size_t)hi << L2) + (size_t)tl * E;
-    slot_fill_contig<E, NT>(st, keyb + ((((size_t)(j * 2 + 0) * A.R + pi)) << logN) + lo, tid);
-    slot_fill_contig<E, NT>(st + EP * NT, keyb + ((((size_t)(j * 2 + 1) * A.R + pi)) << logN) + lo, tid);
-    u32* sp = st + 2 * EP * NT;
-    if (j == own_j) {
-      if (!GALOIS) {
-        slot_fill_contig<E, NT>(sp, xr + lo, tid);
-        if (XMODE == 1) slot_fill_contig<E, NT>(sp + EP * NT, xr2 + lo, tid);
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const u32 src = auto_src_index(((u32)hi << L2) + tl * E + e, gal, logN);
-          cp_async4(sp + slot_idx<E, NT>(e, tid), xr + src);
-          if (XMODE == 1) cp_async4(sp + EP * NT + slot_idx<E, NT>(e, tid), xr2 + src);
-        }
-      }
-    } else {
-      const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
-      slot_fill_contig<E, NT>(sp, tr + (size_t)tl * E, tid);        // line-transposed T1
-    }
-    cp_async_commit();
-  };
-
-  lf_pdl_trigger();
-  stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, LPK, tid, NT);
-  cp_async_commit();
-  lf_pdl_wait();
-  issue(0);
-  u64 accb[E], acca[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) { accb[e] = 0; acca[e] = 0; }
-  const TwTree tw{tws, (1u << L1) + hi0s, LPK};
-  for (int j = 0; j < A.beta; ++j) {
-    if (j + 1 < A.beta) {
-      issue(j + 1);
-      cp_async_wait_group<1>();
-    } else {
-      cp_async_wait_group<0>();
-    }
-    if (j == 0) __syncthreads();                         // twiddles (cooperative) landed
-    const u32* st = stg + (j & 1) * (NSLOT * EP * NT);
-    u32 pc[E];
-    slot_read<E, NT>(pc, st + 2 * EP * NT, tid);
-    if (j == own_j) {
-      // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
-      const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
-      if (XMODE == 1) {
-        u32 w2[E];
-        slot_read<E, NT>(w2, st + 3 * EP * NT, tid);
-#pragma unroll
-        for (int e = 0; e < E; ++e) pc[e] = mulmod(pc[e], w2[e], pk);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) pc[e] = mul_shoup_lazy(pc[e], s, sp, pk.q);
-    } else {
-      fwd_line<L2, BIN>(pc, (1u << L1) + hs, tw, pk.q, xs, tl, addr, SyncWarp{});
-      if (GALOIS) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) perm_buf[tl * E + e] = pc[e];
-        __syncwarp();
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const u32 pos = ((u32)hi << L2) + tl * E + e;
-          pc[e] = perm_buf[auto_src_index(pos, gal, logN) & (M2 - 1)];
-        }
-      }
-    }
-    if (A.beta > 15) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) pc[e] = reduce32_lazy(pc[e], pk);
-    }
-    {
-      u32 kv[E];
-      slot_read<E, NT>(kv, st, tid);
-#pragma unroll
-      for (int e = 0; e < E; ++e) accb[e] += (u64)pc[e] * kv[e];
-      slot_read<E, NT>(kv, st + EP * NT, tid);
-#pragma unroll
-      for (int e = 0; e < E; ++e) acca[e] += (u64)pc[e] * kv[e];
-    }
-    __syncwarp();
-  }
-  u32 rb[E], ra[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) { rb[e] = reduce64(accb[e], pk); ra[e] = reduce64(acca[e], pk); }
-  if (is_main) {
-    store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
-    store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2), tl);
-  } else {
-    const int s = t - l - 1;
-    const uint2* twi = dv.twi + ((size_t)pi << logN);
-    __syncwarp();
-    inv_line<L2>(rb, (1u << L1) + hi, twi, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step2<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
-    __syncwarp();
-    inv_line<L2>(ra, (1u << L1) + hi, twi, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step2<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
-  }
-}
-
 // ---------------------------------------------------------------------------------------
 // K_E: row pass of the NTT of the converted rows, (acc - conv) * scalar, epilogue.
 enum { EPI_KS = 0, EPI_MUL = 1, EPI_ROT = 2 };
@@ -1014,33 +819,11 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.pre = pre ? 1 : 0;
     if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
-#ifndef LF_KSI_PF
-#define LF_KSI_PF 0
-#endif
-    if (LF_KSI_PF && !c.ext_out) {
-    constexpr int LPK = S::LPCR >= 16 ? 8 : S::LPCR;        // lines per CTA (2 CTAs / SM)
-    constexpr int NTK = KsiShape<L2, LPK>::NT;
-    dim3 grid(K.ext * ((1 << L1) / LPK) * c.batch);
-    if (c.op == OP_ROT) {
-      const size_t smK = KsiShape<L2, LPK>::template bytes<3>();
-      lf_smem_optin(k_ks_inner_pf<L1, L2, true, 0, LPK>, smK);
-      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, true, 0, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
-    } else if (c.op == OP_MUL) {
-      const size_t smK = KsiShape<L2, LPK>::template bytes<4>();
-      lf_smem_optin(k_ks_inner_pf<L1, L2, false, 1, LPK>, smK);
-      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, false, 1, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
-    } else {
-      const size_t smK = KsiShape<L2, LPK>::template bytes<3>();
-      lf_smem_optin(k_ks_inner_pf<L1, L2, false, 0, LPK>, smK);
-      LF_LAUNCH_CHECK(lf_launch(k_ks_inner_pf<L1, L2, false, 0, LPK>, dim3(grid), dim3(NTK), smK, s, 1, A, dv));
-    }
-    } else {
     const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
     dim3 grid(K.ext * groups * c.batch);
     if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, true, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
     else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, false, 1>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 1>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
     else { lf_smem_optin(k_ks_inner<L1, L2, false, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
-    }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(3);

@@ -75,23 +75,6 @@ struct TwFlat {
 
 // Stage the subtrees (LP levels) under roots R0..R0+span-1 of table `tab` into smem `dst`
 // (span * (2^LP - 1) entries), cooperatively and coalesced.  Caller syncs afterwards.
-template <int LP>
-LF_DEV void stage_tree(uint2* dst, const uint2* __restrict__ tab, u32 R0, int span, int tid,
-                       int nthr) {
-#pragma unroll
-  for (int d = 0; d < LP; ++d) {
-    const uint2* src = tab + ((size_t)R0 << d);
-    uint2* o = dst + span * ((1 << d) - 1);
-    const int n = span << d;
-    if ((n & 1) == 0 && (((size_t)R0 << d) & 1) == 0 && ((span * ((1 << d) - 1)) & 1) == 0) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(src);
-      uint4* o4 = reinterpret_cast<uint4*>(o);
-      for (int i = tid; i < n / 2; i += nthr) o4[i] = __ldg(&s4[i]);
-    } else {
-      for (int i = tid; i < n; i += nthr) o[i] = __ldg(&src[i]);
-    }
-  }
-}
 // Asynchronous variant (cp.async, no register round trip): the copies land while the thread
 // goes on issuing its data loads; call cp_async_wait_all() + a barrier before reading.
 LF_DEV void cp_async16(void* smem, const void* gmem) {

@@ -81,12 +81,6 @@ class Layout:
         return [(j, x) for j, x in enumerate(g) if x]
 
 
-def shard_rows(rows, ids, lay: Layout, take):
-    """Select this rank's rows of a full (len(ids), N) block (host or device)."""
-    idx = [ids.index(b) for b in lay.local(ids)]
-    return take(rows, idx)
-
-
 class ShardedKeyswitch:
     """keyswitch(x, evk) (ckks.py:134-140) on k ranks with one all-gather per cross-limb stage.
 
