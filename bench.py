@@ -400,10 +400,12 @@ def run_ours(args, rank, world):
     ks_bytes = algorithmic_rows(level) * ROW_BYTES
     achieved_top = stage_info[top]["gbs"]
     traffic = None            # ncu dram bytes of the same kernel, per launch (profiles/, committed)
+    pipes = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
         if top in tr and Bsz == 8 and level == 35:
             traffic = tr[top]["bytes_per_launch"]
+            pipes = {k: tr[top].get(k) for k in ("fmaheavy_pipe_pct", "issue_active_pct", "l1tex_pct", "dram_pct")}
     except Exception:
         pass
 
@@ -495,6 +497,7 @@ def run_ours(args, rank, world):
             "roofline": {"kernel": top, "bound": "hbm", "achieved": achieved_top, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": rows[top] * ROW_BYTES * Bsz,
+                         "ncu_pipes": pipes,
                          "peak_source": peak_src,
                          "note": "algorithmic bytes / CUDA-event time of the launch; traffic = ncu dram read+write of the same launch (profiles/r01_ncu_traffic.json)"},
             "stages": stage_info,

@@ -31,7 +31,13 @@ def main(reps, out):
                 if name.startswith("void " + k) or name.startswith(k):
                     st = s
             if st and st not in res:
-                res[st] = {"bytes_per_launch": tot, "report": rep, "launch": "batch of 8 C2 keyswitches"}
+                def metric(m):
+                    return float(r[h.index(m)]) if m in h and r[h.index(m)] not in ("", "n/a") else None
+                res[st] = {"bytes_per_launch": tot, "report": rep, "launch": "batch of 8 C2 keyswitches",
+                           "fmaheavy_pipe_pct": metric("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                           "issue_active_pct": metric("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                           "l1tex_pct": metric("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                           "dram_pct": metric("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
