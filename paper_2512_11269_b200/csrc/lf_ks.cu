@@ -53,7 +53,8 @@ struct BcArgs {
 template <int L1, int L2, int MODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
-           size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase) {
+           size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase,
+           int nbatch, int bpc) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int GROUPS = (1 << L1) / S::LPCR;
@@ -68,22 +69,31 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   stage_tree_async<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR,
                        threadIdx.x, blockDim.x);
   lf_pdl_wait();
-  const size_t off = (size_t)blockIdx.z * x_bs + ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) +
-                     ((size_t)hi << L2);
-  u32 v[C::E];
-  load_row_step2<L2>(v, x + off, tl);
-  if (MODE == 1) {
-    u32 w[C::E];
-    load_row_step2<L2>(w, x2 + off, tl);
+  // instances blockIdx.z*bpc .. +bpc-1 share the staged twiddles
+  const size_t roff = ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2);
+  const int b0 = blockIdx.z * bpc, b1 = min(nbatch, b0 + bpc);
+#pragma unroll 1
+  for (int b = b0; b < b1; ++b) {
+    const size_t off = (size_t)b * x_bs + roff;
+    u32 v[C::E];
+    load_row_step2<L2>(v, x + off, tl);
+    if (MODE == 1) {
+      u32 w[C::E];
+      load_row_step2<L2>(w, x2 + off, tl);
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
+      for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
+    }
+    if (b + 1 < b1) prefetch_l1(x + off + x_bs + (size_t)tl * C::E);
+    if (b == b0) {
+      cp_async_wait_all();
+      __syncthreads();
+    } else {
+      __syncwarp();
+    }
+    inv_line<L2>(v, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
+                 rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
+    store_row_step2<L2>(v, T0 + (size_t)b * t_bs + ((size_t)row << (L1 + L2)) + ((size_t)hi << L2), tl);
   }
-  cp_async_wait_all();
-  __syncthreads();
-  inv_line<L2>(v, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
-               rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
-  store_row_step2<L2>(v, T0 + (size_t)blockIdx.z * t_bs + ((size_t)row << (L1 + L2)) +
-                             ((size_t)hi << L2), tl);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -523,6 +533,7 @@ struct ModDownArgs {
   const u32* scal;     // per target t: scalar, Shoup companion at scal[t*sstride], +1
   int sstride;
   int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
+  int nbatch, bpc;     // instances; instances per CTA (sharing the staged twiddles)
   u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
 };
 
@@ -548,8 +559,11 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   const TwTree tw{tws, R0, S::LPCR};
   u32* xs = rowpass_xs<L1, L2>(sm);
   const AddrR<L2> addr{ln * pitchR<L2>()};
-  const size_t b = blockIdx.z;
   const size_t lo0 = ((size_t)hi << L2);
+  const int b0 = blockIdx.z * A.bpc, b1 = min(A.nbatch, b0 + A.bpc);
+#pragma unroll 1
+  for (int bb = b0; bb < b1; ++bb) {
+  const size_t b = bb;
 #pragma unroll 1
   for (int p = 0; p < 2; ++p) {
     u32 cv[C::E], av[C::E];
@@ -559,7 +573,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
       prefetch_l1(A.acc + b * A.acc_bs + ((size_t)t << logN) + lo0 + (size_t)tl * C::E);
       prefetch_l1(A.acc + b * A.acc_bs + ((size_t)(A.nacc + t) << logN) + lo0 + (size_t)tl * C::E);
     }
-    if (p) {
+    if (p || bb != b0) {
       __syncwarp();
     } else {
       cp_async_wait_all();
@@ -602,6 +616,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
       }
     }
     store_row_step2<L2>(av, A.out + b * A.out_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
+  }
   }
 }
 
@@ -775,11 +790,15 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   LF_MARK(0);
   // K_A
   {
-    dim3 grid(l1 * groups, 1, nsh);
+#ifndef LF_BPC
+#define LF_BPC 4
+#endif
+    const int bpc_in = nsh >= 2 * LF_BPC ? LF_BPC : 1;      // instances per CTA (shared twiddles)
+    dim3 grid(l1 * groups, 1, (nsh + bpc_in - 1) / bpc_in);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in)); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -852,7 +871,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1;
     for (int b = 0; b < c.batch; ++b) A.gs[b] = c.g_of(b);
-    dim3 grid(l1 * groups, 1, c.batch);
+    A.nbatch = c.batch;
+    A.bpc = c.batch >= 2 * LF_BPC ? LF_BPC : 1;
+    dim3 grid(l1 * groups, 1, (c.batch + A.bpc - 1) / A.bpc);
     if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_MUL>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_ROT>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
@@ -884,7 +905,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt, batch, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -902,6 +923,8 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
     A.t3_bs = per; A.acc_bs = ct_bs; A.out_bs = out_bs; A.e_bs = 0;
     A.scal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)l * P->n_main * 2; A.sstride = 2;
     A.nt = nt; A.nacc = l + 1; A.ne = 0;
+    A.nbatch = batch;
+    A.bpc = 1;
     dim3 grid(nt * groups, 1, batch);
     { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
@@ -926,7 +949,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
   u32* T3 = T2 + 2 * (size_t)alpha * N;
   {
     dim3 grid(2 * alpha * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -949,6 +972,8 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
     A.T3 = T3; A.acc = in; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
     A.t3_bs = per; A.acc_bs = in_bs; A.out_bs = out_bs; A.e_bs = 0;
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = ext; A.ne = 0;
+    A.nbatch = batch;
+    A.bpc = 1;
     dim3 grid(l1 * groups, 1, batch);
     { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
@@ -969,7 +994,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
