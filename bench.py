@@ -311,6 +311,38 @@ def sharded_keyswitch_latency(params, level, rlk, rank, world, dev, reps=10):
             "path": "shard.gpu_sharded_keyswitch (row kernels + 2 all-gathers; not the fused pipeline)"}
 
 
+def batch_sweep(params, level, rlk, dev, batches=(1, 8), steps=5):
+    """Per-keyswitch time at other batch sizes of SURVEY §8d C2 (B in {1, 8, 32}): same
+    synthetic inputs, L2 flushed between steps, CUDA events."""
+    import torch
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.context import get_context
+    ctx = get_context(params)
+    l1 = level + 1
+    q = torch.tensor(params.rns_basis[:l1], dtype=torch.int64, device=dev)[:, None]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    out = {}
+    for B in batches:
+        g = torch.Generator(device=dev).manual_seed(77 + B)
+        x = (torch.randint(0, 2 ** 62, (B, l1, params.N), device=dev, generator=g, dtype=torch.int64) % q).to(torch.int32)
+        o = torch.empty((B, 2, l1, params.N), dtype=torch.int32, device=dev)
+        ws = ctx.ks_workspace(level, B)
+        for _ in range(2):
+            fused.keyswitch_batch(params, level, x, rlk, out=o, ws=ws)
+        ms = 0.0
+        for i in range(steps):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fused.keyswitch_batch(params, level, x, rlk, out=o, ws=ws)
+            b.record()
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        out[str(B)] = {"keyswitch_us": ms / steps / B * 1e3}
+        del x, o, ws
+    return out
+
+
 def ntt_summary(ntt, clocks):
     mhz = (clocks or {}).get("sm_mhz") or 1965
     peak = 32 * 148 * mhz * 1e6                  # IMAD.HI per second (one per butterfly)
@@ -403,7 +435,7 @@ def run_ours(args, rank, world):
     pipes = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
-        if top in tr and Bsz == 8 and level == 35:
+        if top in tr and tr[top].get("batch", 8) == Bsz and level == 35:
             traffic = tr[top]["bytes_per_launch"]
             pipes = {k: tr[top].get(k) for k in ("fmaheavy_pipe_pct", "issue_active_pct", "l1tex_pct", "dram_pct")}
     except Exception:
@@ -471,6 +503,7 @@ def run_ours(args, rank, world):
                "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
 
     ntt = ntt_throughput(params, dev)
+    sweep = batch_sweep(params, level, rlk, dev) if rank == 0 else None
 
     sharded = None
     if world > 1:
@@ -509,6 +542,7 @@ def run_ours(args, rank, world):
             "cpu_baseline": cpu,
             "bootstrap": boot,
             "ntt": ntt_summary(ntt, clocks),
+            "batch_sweep": sweep,
             "limb_sharded": sharded,
         }
         print(json.dumps(line), flush=True)
@@ -519,7 +553,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--level", type=int, default=35)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")

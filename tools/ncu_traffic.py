@@ -9,7 +9,7 @@ import sys
 STAGE_OF = [("k_modup_in", "modup_in"), ("k_ks_inner", "ks_inner"), ("k_moddown_out", "moddown_out")]
 
 
-def main(reps, out):
+def main(reps, out, batch=8):
     res = {}
     for rep in reps:
         txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -33,7 +33,7 @@ def main(reps, out):
             if st and st not in res:
                 def metric(m):
                     return float(r[h.index(m)]) if m in h and r[h.index(m)] not in ("", "n/a") else None
-                res[st] = {"bytes_per_launch": tot, "report": rep, "launch": "batch of 8 C2 keyswitches",
+                res[st] = {"bytes_per_launch": tot, "report": rep, "launch": f"batch of {batch} C2 keyswitches", "batch": batch,
                            "fmaheavy_pipe_pct": metric("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                            "issue_active_pct": metric("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                            "l1tex_pct": metric("l1tex__throughput.avg.pct_of_peak_sustained_active"),
@@ -43,4 +43,8 @@ def main(reps, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:-1], sys.argv[-1])
+    args = sys.argv[1:]
+    batch = 8
+    if args and args[0].startswith("--batch="):
+        batch = int(args.pop(0).split("=")[1])
+    main(args[:-1], args[-1], batch)
