@@ -47,7 +47,7 @@ def main(rep):
                 else:
                     x = float(v.replace(",", ""))
                     if key.startswith("gpu__time"):
-                        x *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(units[i], 1.0)
+                        x *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(units[i], 1.0)
                     cells.append(f"{x:.1f}" if x < 1e6 else f"{x:.3g}")
             except ValueError:
                 cells.append(v)
