@@ -458,6 +458,7 @@ def run_ours(args, rank, world):
         start.record(stream)
         s_h2d.wait_event(start)
         last = None
+        keep = []            # results stay referenced until the step's D2H copies are enqueued and joined
         for b in range(Bsz):
             ev_in = torch.cuda.Event()
             with torch.cuda.stream(s_h2d):
@@ -468,14 +469,15 @@ def run_ours(args, rank, world):
             ev_out = torch.cuda.Event()
             ev_out.record(stream)
             s_d2h.wait_event(ev_out)
+            keep.append((kb, ka))
             with torch.cuda.stream(s_d2h):
-                kb.limbs.record_stream(s_d2h)
-                ka.limbs.record_stream(s_d2h)
                 host_out[b, 0].copy_(kb.limbs, non_blocking=True)
                 host_out[b, 1].copy_(ka.limbs, non_blocking=True)
                 last = torch.cuda.Event()
                 last.record(s_d2h)
         stream.wait_event(last)
+        last.synchronize()
+        keep.clear()
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
