@@ -435,6 +435,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       // finished piece: load the source line, permute inside it (sigma_g) through smem
       load_row_step2<L2>(pc, A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2), tl);
       if (GALOIS) {
+        __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
         for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
         __syncwarp();
@@ -463,6 +464,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
                         tl, addr, SyncWarp{});
       if (GALOIS) {
+        __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
         for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
         __syncwarp();

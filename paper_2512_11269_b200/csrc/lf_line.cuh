@@ -24,6 +24,7 @@
 // below 16q < 2^32.  The bound is tracked at compile time (units of q).  The inverse uses
 // Harvey's butterfly with inputs/outputs in [0, 2q).
 #pragma once
+#include <type_traits>
 #include "lf_arith.cuh"
 
 template <int LP>
@@ -166,9 +167,26 @@ struct FwdLineBound {
 
 // Exchange helpers.  `Addr` maps a line position to a shared-memory word index for the
 // calling thread's line.  Sync is the barrier covering all threads of a line.
+// A warp-synchronous exchange buffer is reused by the next line transform of the same warp, so
+// the writes must not overtake the previous reads of other lanes: sync first (the CUDA model
+// does not guarantee lockstep; compute-sanitizer racecheck flags the WAR otherwise).  Block /
+// group barriers are placed by the calling kernels.
+struct SyncBlock {
+  LF_DEV void operator()() const { __syncthreads(); }
+};
+struct SyncWarp {
+  LF_DEV void operator()() const { __syncwarp(__activemask()); }
+};
+
+template <class Sync>
+LF_DEV void xchg_pre(Sync sync) {
+  if constexpr (std::is_same<Sync, SyncWarp>::value) sync();
+}
+
 template <int LP, class Addr, class Sync>
 LF_DEV void xchg_12(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
   using C = LineCfg<LP>;
+  xchg_pre(sync);
 #pragma unroll
   for (int j = 0; j < C::E; ++j) sm[addr(tl + C::T * j)] = x[j];
   sync();
@@ -179,6 +197,7 @@ LF_DEV void xchg_12(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
 template <int LP, class Addr, class Sync>
 LF_DEV void xchg_21(u32* x, u32* sm, int tl, Addr addr, Sync sync) {
   using C = LineCfg<LP>;
+  xchg_pre(sync);
 #pragma unroll
   for (int e = 0; e < C::E; ++e) sm[addr(tl * C::E + e)] = x[e];
   sync();

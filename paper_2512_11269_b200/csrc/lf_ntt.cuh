@@ -14,12 +14,6 @@ struct AddrR {
   int base;
   LF_DEV int operator()(int p) const { return base + p + (p >> LineCfg<LP>::LA); }
 };
-struct SyncBlock {
-  LF_DEV void operator()() const { __syncthreads(); }
-};
-struct SyncWarp {
-  LF_DEV void operator()() const { __syncwarp(__activemask()); }
-};
 
 template <int LP, int CW>
 __host__ __device__ constexpr int smemC_words() {
