@@ -503,6 +503,13 @@ class Bootstrapper:
         return y
 
     # -- the pipeline ----------------------------------------------------------------
+    def _mark(self, name):
+        if getattr(self, "marks", None) is not None:
+            import torch
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.marks.append((name, e))
+
     def bootstrap(self, ct, out_scale=None):
         """Refresh a level-0 ciphertext; returns a ciphertext at level
         L - (2 cts_levels - 1) - 2 (EvalMod depth) - (stc_levels + 1) with scale `out_scale`
@@ -512,7 +519,9 @@ class Bootstrapper:
             ct = be.drop_to_level(ct, 0)
         delta_in = Fraction(ct.scale)
         q = self.q
+        self._mark("start")
         x = be.mod_raise(ct)                                  # level L, scale Delta_in
+        self._mark("modraise")
         # Lift the integers to a ~2^52 scale with an exact integer multiplication (no level):
         # the keyswitch and rescale noise of CoeffToSlot is absolute, the slots are dominated
         # by q0*I, and m/q0 must survive at ~2^-40 relative precision.
@@ -532,13 +541,16 @@ class Bootstrapper:
                 lo = l - 2
                 S_p = Fraction(q[lo]) * q[lo - 1] * q[l] * q[l - 1] / Fraction(x.scale)
                 x = self._linear(x, plan, ("cts", i, float(delta_in)), c0, S_p, 2)
+        self._mark("coeff_to_slot")
         # conjugation split (both EvalMod inputs carry the same level and scale)
         xc = be.conjugate(x)
         re = be.add(x, xc)
         im = be.mul_monomial(be.sub(x, xc), 3 * self.N // 2)   # * (-i) = * X^(3N/2)
         re = be.add_const(re, self.beta)
         im = be.add_const(im, self.beta)
+        self._mark("conj_split")
         re, im = be.unstack(self._evalmod(be.stack([re, im])))   # both parts in one batch
+        self._mark("evalmod")
         y = be.add(re, be.mul_monomial(im, self.N // 2))       # re + i im
         # SlotToCoeff: the first level folds q0/Delta_in, the last lands on out_scale
         out_scale = Fraction(self.out_scale if out_scale is None else out_scale)
@@ -553,6 +565,7 @@ class Bootstrapper:
             else:
                 S_p = out_scale * q[l] * q[l - 1] / Fraction(y.scale)
                 y = self._linear(y, plan, tag, const, S_p, 2)
+        self._mark("slot_to_coeff")
         return y
 
 

@@ -78,3 +78,11 @@ if "--graph" in sys.argv:
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
     print("graph bootstrap ms:", [round(x, 2) for x in ms])
+
+if "--phases" in sys.argv:
+    bt.marks = []
+    bt.bootstrap(ct)
+    torch.cuda.synchronize()
+    m = bt.marks
+    bt.marks = None
+    print("phases (eager, ms):", {b[0]: round(a[1].elapsed_time(b[1]), 2) for a, b in zip(m, m[1:])})
