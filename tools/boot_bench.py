@@ -13,9 +13,10 @@ from paper_2512_11269_b200 import bootstrap as BT  # noqa: E402
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 47
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 t0 = time.time()
-p = B.gen_params(65536, L, d=4, seed=0, scale=2 ** 26)
+dnum = int(next((a.split("=")[1] for a in sys.argv if a.startswith("dnum=")), 4))
+p = B.gen_params(65536, L, d=dnum, seed=0, scale=2 ** 26)
 sk, pk, rlk = B.keygen(p, seed=11)
-cfg = BT.BootConfig(**{k: int(v) for k, v in (a.split("=") for a in sys.argv[3:] if "=" in a)})
+cfg = BT.BootConfig(**{k: int(v) for k, v in (a.split("=") for a in sys.argv[3:] if "=" in a and not a.startswith("dnum="))})
 print("config", cfg)
 planner = BT.Bootstrapper(type("P", (), {"N": p.N, "main_primes": p.rns_basis}), cfg)
 rots = planner.required_rotations()
