@@ -506,7 +506,9 @@ class Bootstrapper:
     def _mark(self, name):
         if getattr(self, "marks", None) is not None:
             import torch
-            e = torch.cuda.Event(enable_timing=True)
+            # external events become event-record nodes when the pipeline is being captured
+            e = torch.cuda.Event(enable_timing=True,
+                                 external=torch.cuda.is_current_stream_capturing())
             e.record()
             self.marks.append((name, e))
 
@@ -588,10 +590,15 @@ class ExtCt:
 
 class CtBatch:
     """B ciphertexts at one level and scale in one (B, 2, level+1, N) device tensor; the GPU
-    backend runs every operation on all of them in one batched launch."""
+    backend runs every operation on all of them in one batched launch.  `data` may be a
+    row-prefix view of a higher-level batch (drop_to_level does not copy); `dense()` gives a
+    contiguous batch for the calls whose C-ABI takes one instance stride."""
 
     def __init__(self, data, scale, level):
         self.data, self.scale, self.level = data, Fraction(scale), level
+
+    def dense(self):
+        return self if self.data.is_contiguous() else CtBatch(self.data.contiguous(), self.scale, self.level)
 
 
 def map_batch(fn, *args):
@@ -660,7 +667,7 @@ class GpuBackend:
         if ct.level == level:
             return ct
         if isinstance(ct, CtBatch):
-            return CtBatch(ct.data[:, :, : level + 1].contiguous(), ct.scale, level)
+            return CtBatch(ct.data[:, :, : level + 1], ct.scale, level)       # a view
         assert level < ct.level
         from .poly import RnsPolynomial, main_ids
         ids = main_ids(level)
@@ -803,6 +810,7 @@ class GpuBackend:
         import torch
         from .poly import ewise
         assert x.level == y.level and x.scale == y.scale and x.data.shape == y.data.shape
+        x, y = x.dense(), y.dense()
         out = torch.empty_like(x.data)
         n = x.data.shape[0] * 2 * (x.level + 1)
         ewise(self.params, op, out.view(n, -1), x.data.view(n, -1), self._rows_pidx(x), b=y.data.view(n, -1))
@@ -834,6 +842,7 @@ class GpuBackend:
             from . import _native
             from .context import dptr, get_context, stream_handle
             ctx = get_context(self.params)
+            x = x.dense()
             B = x.data.shape[0]
             ws = ctx.rescale_workspace(x.level, B)
             out = torch.empty((B, 2, x.level - 1, self.params.N), dtype=torch.int32, device=x.data.device)
@@ -851,6 +860,7 @@ class GpuBackend:
             from . import _native
             from .context import dptr, get_context, stream_handle
             assert x.level == y.level and x.data.shape == y.data.shape and x.level >= 1
+            x, y = x.dense(), y.dense()
             ctx = get_context(self.params)
             B = x.data.shape[0]
             ws = ctx.ks_workspace(x.level, B)
@@ -864,13 +874,16 @@ class GpuBackend:
     def conjugate(self, x):
         return self.C.hom_conjugate(x, self.ck, self.params)
 
-    def lincomb(self, terms):
+    def lincomb(self, terms, out=None):
         """sum_i round(c_i S_i) * ct_i, all ct_i at one level with equal ct_i.scale * S_i."""
         import torch
         if isinstance(terms[0][0], CtBatch):
-            B = terms[0][0].data.shape[0]
-            outs = [self.lincomb([(self.unstack(t)[i], c, S) for t, c, S in terms]) for i in range(B)]
-            return self.stack(outs)
+            t0 = terms[0][0]
+            B = t0.data.shape[0]
+            out = torch.empty((B, 2, t0.level + 1, self.N), dtype=torch.int32, device=t0.data.device)
+            for i in range(B):       # per instance, straight into the batch (views, no copies)
+                self.lincomb([(self.unstack(t)[i], c, S) for t, c, S in terms], out=out[i])
+            return CtBatch(out, Fraction(t0.scale) * Fraction(terms[0][2]), t0.level)
         from . import _native
         from .context import get_context, stream_handle
         from .poly import Domain, RnsPolynomial, main_ids
@@ -879,7 +892,7 @@ class GpuBackend:
         scale = Fraction(ct0.scale) * Fraction(terms[0][2])
         nrows = level + 1
         qs = self.params.rns_basis[:nrows]
-        out = None
+        dst, out = out, None
         ctx = get_context(self.params)
         for i0 in range(0, len(terms), 8):
             chunk = terms[i0: i0 + 8]
@@ -889,14 +902,19 @@ class GpuBackend:
                 assert ct.level == level and Fraction(ct.scale) * Fraction(S) == scale
                 k = round(Fraction(c) * Fraction(S))
                 ks.extend(k % q for q in qs)
-            tgt = torch.empty((2, nrows, self.params.N), dtype=torch.int32, device=ct0.b.limbs.device)
+            tgt = dst if (i0 == 0 and dst is not None) else \
+                torch.empty((2, nrows, self.params.N), dtype=torch.int32, device=ct0.b.limbs.device)
             bp = (ctypes_void_p * n)(*[ct.b.limbs.data_ptr() for ct, _, _ in chunk])
             ap = (ctypes_void_p * n)(*[ct.a.limbs.data_ptr() for ct, _, _ in chunk])
             from . import _native as nat
             _native.check(nat.lib().lf_lincomb(ctx.handle, ctypes_void_p(tgt.data_ptr()), nrows, n, bp, ap,
                                                nat.u32_array(ks), stream_handle()), "lf_lincomb")
-            out = tgt if out is None else torch.stack([self._addrows(out[0], tgt[0], level),
-                                                        self._addrows(out[1], tgt[1], level)])
+            if out is None:
+                out = tgt
+            else:
+                from .poly import LF_OP_ADD, ewise
+                for p in range(2):
+                    ewise(self.params, LF_OP_ADD, out[p], out[p], main_ids(level), b=tgt[p])
         ids = main_ids(level)
         return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
                                  RnsPolynomial(out[1], Domain.EVAL, ids), scale, level)
@@ -988,10 +1006,16 @@ class GpuBackend:
         ids = main_ids(ct.level)
         sc = self._scalar_rows(ct, k)
         if isinstance(ct, CtBatch):
-            n = ct.data.shape[0] * 2 * (ct.level + 1)
-            out = torch.empty_like(ct.data)
-            ewise(self.params, LF_OP_SCALAR_MUL, out.view(n, -1), ct.data.view(n, -1), self._rows_pidx(ct),
-                  scalars=sc * (2 * ct.data.shape[0]))
+            B = ct.data.shape[0]
+            out = torch.empty((B, 2, ct.level + 1, self.N), dtype=torch.int32, device=ct.data.device)
+            if ct.data.is_contiguous():
+                n = B * 2 * (ct.level + 1)
+                ewise(self.params, LF_OP_SCALAR_MUL, out.view(n, -1), ct.data.view(n, -1),
+                      self._rows_pidx(ct), scalars=sc * (2 * B))
+            else:                    # a dropped view: per polynomial, its rows are contiguous
+                for i in range(B):
+                    for p in range(2):
+                        ewise(self.params, LF_OP_SCALAR_MUL, out[i, p], ct.data[i, p], ids, scalars=sc)
             return CtBatch(out, ct.scale * Fraction(S_p), ct.level)
         out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
         ewise(self.params, LF_OP_SCALAR_MUL, out[0], ct.b.limbs, ids, scalars=sc)
@@ -1006,6 +1030,7 @@ class GpuBackend:
         k = round(Fraction(c) * Fraction(ct.scale))
         ids = main_ids(ct.level)
         if isinstance(ct, CtBatch):
+            ct = ct.dense()
             B = ct.data.shape[0]
             n = B * 2 * (ct.level + 1)
             sc = (self._scalar_rows(ct, k) + [0] * (ct.level + 1)) * B       # b rows only

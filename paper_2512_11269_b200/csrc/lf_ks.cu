@@ -227,7 +227,10 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const int ct = bid % NCT;
   const BcGroupDev& G = A.g[bid / NCT];
   const BconvDev& B = G.B;
-  const int k = KEX > 0 ? KEX : B.k;
+  // k: this group's sources; kw: sources the MAC loop runs over (KEX pads smaller groups of
+  // a non-uniform launch with zero tiles and zero weights)
+  const int k = B.k;
+  const int kw = KEX > 0 ? KEX : k;
   const int col = ct * CW + c;
   u32* Ybase = sm + (size_t)(tl * CW + c) * E;
   u32* X = sm + (size_t)kmax * YI + grp * smemC_words<L1, CW>();
@@ -241,14 +244,28 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   const int chunk = (B.m + A.tsplit - 1) / A.tsplit;
   const int t0 = ts * chunk, t1 = min(B.m, t0 + chunk);
   lf_pdl_trigger();
-  for (int w = threadIdx.x; w < (t1 - t0) * k; w += blockDim.x) Wsm[w] = __ldg(&B.w[(size_t)t0 * k + w]);
+  if (kw == k) {
+    for (int w = threadIdx.x; w < (t1 - t0) * k; w += blockDim.x) Wsm[w] = __ldg(&B.w[(size_t)t0 * k + w]);
+  } else {
+    for (int w = threadIdx.x; w < (t1 - t0) * kw; w += blockDim.x) {
+      const int tt = w / kw, i = w - tt * kw;
+      Wsm[w] = i < k ? __ldg(&B.w[(size_t)(t0 + tt) * k + i]) : 0u;
+    }
+  }
   lf_pdl_wait();
 
   // phase 1: INTT column pass of each source row, sources split over the groups and (when the
   // target range is split over a cluster) over the cluster's CTAs; the other CTAs' converted
   // source tiles are then pulled through distributed shared memory instead of recomputed.
   const int cl = A.tsplit;
-  for (int i = ts + cl * grp; i < k; i += cl * TG) {
+  for (int i = ts + cl * grp; i < kw; i += cl * TG) {
+    if (i >= k) {                                      // padding tile (block-uniform branch)
+      u32 z[E];
+#pragma unroll
+      for (int j = 0; j < E; ++j) z[j] = 0;
+      y_store<E>(Ybase + (size_t)i * YI, z, rot);
+      continue;
+    }
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
@@ -262,7 +279,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
   }
   if (cl > 1) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    for (int i = 0; i < k; ++i) {
+    for (int i = 0; i < kw; ++i) {
       const int r = i % cl;
       if (r == ts) continue;
       for (int v = threadIdx.x; v < YI / 4; v += blockDim.x) {
@@ -325,7 +342,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     const int pi = B.tgt_pi[t];
     const PrimeK pk = dv.pk[pi];
     const u32 ns = B.negS[t];
-    const u32* wrow = Wsm + (t - t0) * k;
+    const u32* wrow = Wsm + (t - t0) * kw;
     constexpr int EH = E >= 16 ? E / 2 : E;
     u32 x[E];
 #pragma unroll
@@ -334,7 +351,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 #pragma unroll
       for (int j = 0; j < EH; ++j)
         acc[j] = (u64)((up[(h * EH + j) / 4] >> (8 * ((h * EH + j) % 4))) & 0xFFu) * ns;
-      bconv_mac<E, EH, KEX, YI>(acc, yq, wrow, k, Ybase, h);
+      bconv_mac<E, EH, KEX, YI>(acc, yq, wrow, kw, Ybase, h);
 #pragma unroll
       for (int j = 0; j < EH; ++j) x[h * EH + j] = reduce64_lazy4(acc[j], pk);
     }
@@ -718,8 +735,8 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
 
 // Column tile width and group count: CW = 8 columns (32-byte row segments) and four thread
 // groups sharing the source tile for the production sizes; narrower tiles for large digit
-// counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches whose groups all
-// have the same source count 1..12 use the compile-time-K kernel.
+// counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches with at most 12
+// sources per group use the compile-time-K kernel.
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   constexpr int NCOL = 1 << L2;
@@ -727,16 +744,13 @@ static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax
   constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 4 : 1;
   if (kmax > 16) return launch_bc<L1, L2, (NCOL >= 2 ? 2 : 1), 64, 1, 0>(ctx, A, batch, kmax, s);
   if constexpr (L1 == 8 && L2 == 8) {
-    bool uniform = true;
-    for (int g = 0; g < A.ngroups; ++g) uniform &= A.g[g].B.k == kmax;
-    if (uniform) {
-      switch (kmax) {
+    // groups with fewer sources than kmax (uneven digits) run padded with zero tiles
+    switch (kmax) {
 #define LF_BC_K(K) case K: return launch_bc<L1, L2, CW8, 16, TG, K>(ctx, A, batch, kmax, s);
-        LF_BC_K(1) LF_BC_K(2) LF_BC_K(3) LF_BC_K(4) LF_BC_K(5) LF_BC_K(6) LF_BC_K(7) LF_BC_K(8) LF_BC_K(9)
-        LF_BC_K(10) LF_BC_K(11) LF_BC_K(12)
+      LF_BC_K(1) LF_BC_K(2) LF_BC_K(3) LF_BC_K(4) LF_BC_K(5) LF_BC_K(6) LF_BC_K(7) LF_BC_K(8) LF_BC_K(9)
+      LF_BC_K(10) LF_BC_K(11) LF_BC_K(12)
 #undef LF_BC_K
-        default: break;
-      }
+      default: break;
     }
   }
   return launch_bc<L1, L2, CW8, 16, TG, 0>(ctx, A, batch, kmax, s);

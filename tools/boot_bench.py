@@ -56,6 +56,30 @@ if "--profile" in sys.argv:
     print(f"kernel time total {tot / 1e3:.2f} ms over {sum(k.count for k in ka)} launches")
     print(ka.table(sort_by="device_time_total", row_limit=15))
 
+for phase in ("_evalmod", "_linear"):
+    if f"--profile{phase}" not in sys.argv:
+        continue
+    # record the phase's inputs during one bootstrap, then profile the phase alone
+    from torch.profiler import ProfilerActivity, profile
+    orig, calls = getattr(bt, phase), []
+
+    def rec(*a, _o=orig, **k):
+        calls.append((a, k))
+        return _o(*a, **k)
+    setattr(bt, phase, rec)
+    bt.bootstrap(ct)
+    setattr(bt, phase, orig)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for a, k in calls:
+            orig(*a, **k)
+        torch.cuda.synchronize()
+    ka = prof.key_averages()
+    tot = sum(k.device_time_total for k in ka)
+    print(f"{phase}: {len(calls)} calls, kernel time {tot / 1e3:.2f} ms over "
+          f"{sum(k.count for k in ka)} launches")
+    print(ka.table(sort_by="device_time_total", row_limit=25))
+
 if "--graph" in sys.argv:
     static_in = ct
     g = torch.cuda.CUDAGraph()
@@ -64,8 +88,11 @@ if "--graph" in sys.argv:
     with torch.cuda.stream(s):
         bt.bootstrap(static_in)
     torch.cuda.current_stream().wait_stream(s)
+    if "--phases" in sys.argv:
+        bt.marks = []
     with torch.cuda.graph(g):
         gout = bt.bootstrap(static_in)
+    gmarks, bt.marks = bt.marks, None
     g.replay()
     torch.cuda.synchronize()
     dg = B.decrypt(gout, sk, p)
@@ -79,6 +106,9 @@ if "--graph" in sys.argv:
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
     print("graph bootstrap ms:", [round(x, 2) for x in ms])
+    if gmarks:
+        print("phases (graph, ms):", {b[0]: round(a[1].elapsed_time(b[1]), 2)
+                                      for a, b in zip(gmarks, gmarks[1:])})
 
 if "--phases" in sys.argv:
     bt.marks = []
