@@ -116,6 +116,14 @@ int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t
                size_t ct_bstride, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
                int batch, void* workspace, void* stream);
 
+/* hom_mul followed by ndrop in {1, 2} rescales (ckks.py:182-194, then ckks.py:220-225 ndrop
+ * times), bit for bit, with the rescale folded into the relinearisation's ModDown: one exact
+ * floor division by P q_level [q_level-1] instead of a division by P and a second pass.
+ * out = 2 x (level + 1 - ndrop) rows; workspace as lf_keyswitch. */
+int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
+                       const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
+                       size_t out_bstride, int batch, void* workspace, void* stream);
+
 /* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
  * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a
  * rotation, 2N-1 for conjugation. */

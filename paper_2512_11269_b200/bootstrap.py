@@ -408,6 +408,12 @@ class Bootstrapper:
         be = self.be
         lv = min(a.level, b.level)
         a, b = be.drop_to_level(a, lv), be.drop_to_level(b, lv)
+        return self._mulr2(a, b)
+
+    def _mulr2(self, a, b):
+        be = self.be
+        if hasattr(be, "mul_rescale2"):
+            return be.mul_rescale2(a, b)
         return be.rescale2(be.hom_mul(a, b))
 
     def _cheb_powers(self, u):
@@ -480,7 +486,7 @@ class Bootstrapper:
         TG = be.drop_to_level(T[G], m)
         q_scale = Fraction(scale) * self.q[m] * self.q[m - 1] / Fraction(TG.scale)
         qc = self._cheb_eval(q, T, m, q_scale)
-        prod = be.rescale2(be.hom_mul(qc, TG))
+        prod = self._mulr2(qc, TG)
         assert prod.level == level and prod.scale == scale
         rc = self._cheb_eval(r, T, level, scale)
         return be.add(prod, rc)
@@ -853,6 +859,37 @@ class GpuBackend:
         b, a = fused.rescale_multi(self.params, x, 2)
         q = self.params.rns_basis
         return self.C.Ciphertext(b, a, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
+
+    def mul_rescale2(self, x, y):
+        """rescale2(hom_mul(x, y)) in one pipeline (lf_hom_mul_rescale, ndrop 2)."""
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        assert x.level == y.level and x.level >= 2
+        q = self.params.rns_basis
+        scale = x.scale * y.scale / q[x.level] / q[x.level - 1]
+        ctx = get_context(self.params)
+        if isinstance(x, CtBatch):
+            x, y = x.dense(), y.dense()
+            assert x.data.shape == y.data.shape
+            B = x.data.shape[0]
+            c1, c2 = x.data, y.data
+        else:
+            from .fused import ct_block
+            B = 1
+            c1, c2 = ct_block(x), ct_block(y)
+        ws = ctx.ks_workspace(x.level, B)
+        out = torch.empty((B, 2, x.level - 1, self.N), dtype=torch.int32, device=c1.device)
+        _native.check(_native.lib().lf_hom_mul_rescale(ctx.handle, x.level, 2, dptr(c1), dptr(c2),
+                                                       c1.numel() // B, dptr(self.rlk.data), dptr(out),
+                                                       out[0].numel(), B, dptr(ws), stream_handle()),
+                      "lf_hom_mul_rescale")
+        if isinstance(x, CtBatch):
+            return CtBatch(out, scale, x.level - 2)
+        from .poly import Domain, RnsPolynomial, main_ids
+        ids = main_ids(x.level - 2)
+        return self.C.Ciphertext(RnsPolynomial(out[0, 0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[0, 1], Domain.EVAL, ids), scale, x.level - 2)
 
     def hom_mul(self, x, y):
         if isinstance(x, CtBatch):

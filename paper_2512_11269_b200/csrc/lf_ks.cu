@@ -380,6 +380,12 @@ struct KsInnerArgs {
                        //    into acc (2 x ext rows per instance) and skip ModDown (hoisted-ModDown BSGS)
   const u32* eb;       // ext_out: ct.b rows (shared by all instances), P mod q_t table
   const u32* pmod;
+  int fuse_nd;         // tensor mode fused with a rescale by fuse_nd primes: the top fuse_nd main
+                       // rows get + P*(d0, d1) and join the special rows in T2 (t2_rows per poly)
+  int t2_rows;
+  const u32 *c1, *c2;  // fuse_nd: ct1, ct2 (b rows then a rows, c_ne rows per poly)
+  size_t c_bs;
+  int c_ne;
   const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
   u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
 };
@@ -524,18 +530,42 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     }
     store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
     store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(ext + t) << logN) + ((size_t)hi << L2), tl);
-  } else if (is_main) {
+  } else if (is_main && t <= l - A.fuse_nd) {
     store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
     store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2), tl);
   } else {
-    const int s = t - l - 1;
+    // special row, or (fused rescale) one of the top main rows: T2 holds the rows the division
+    // by P q_l [q_{l-1}] converts, in coefficient form after the row pass of the INTT
+    const int s = is_main ? A.alpha + (t - (l + 1 - A.fuse_nd)) : t - l - 1;
+    if (XMODE == 1 && is_main) {
+      // + P * (d0, d1) (ckks.py:189-193: d0 = b1 b2, d1 = b1 a2 + a1 b2) before the division
+      const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
+      const u32* c1 = A.c1 + b * A.c_bs;
+      const u32* c2 = A.c2 + b * A.c_bs;
+      const size_t lo = (size_t)hi << L2;
+      u32 b1[C::E], b2[C::E], o[C::E];
+      load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo, tl);
+      load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo, tl);
+#pragma unroll
+      for (int e = 0; e < C::E; ++e)
+        rb[e] = addmod(rb[e], mul_shoup(mulmod(b1[e], b2[e], pk), pm, pmp, pk.q), pk.q);
+      load_row_step2<L2>(o, c2 + ((size_t)(A.c_ne + t) << logN) + lo, tl);      // a2
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) b1[e] = mulmod(b1[e], o[e], pk);          // b1 a2
+      load_row_step2<L2>(o, c1 + ((size_t)(A.c_ne + t) << logN) + lo, tl);      // a1
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) {
+        const u32 d1 = addmod(b1[e], mulmod(o[e], b2[e], pk), pk.q);
+        ra[e] = addmod(ra[e], mul_shoup(d1, pm, pmp, pk.q), pk.q);
+      }
+    }
     const uint2* tw = dv.twi + ((size_t)pi << logN);
     __syncwarp();
     inv_line<L2>(rb, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
     store_row_step2<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);
     __syncwarp();
     inv_line<L2>(ra, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
-    store_row_step2<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.alpha + s) << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.T2 + b * A.t2_bs + ((size_t)(A.t2_rows + s) << logN) + ((size_t)hi << L2), tl);
   }
 }
 
@@ -551,6 +581,7 @@ struct ModDownArgs {
   size_t t3_bs, acc_bs, out_bs, e_bs;
   const u32* scal;     // per target t: scalar, Shoup companion at scal[t*sstride], +1
   int sstride;
+  const u32* dscal;    // EPI_MUL fused with a rescale: (q_l [q_{l-1}])^-1 for the d terms, stride 2
   int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
   int nbatch, bpc;     // instances; instances per CTA (sharing the staged twiddles)
   u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
@@ -612,15 +643,21 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
       u32 b1[C::E], b2[C::E], o1[C::E], o2[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo0, tl);
       load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo0, tl);
+      const u32 ds = A.dscal ? A.dscal[2 * t] : 0u, dsp = A.dscal ? A.dscal[2 * t + 1] : 0u;
       if (p == 0) {
 #pragma unroll
-        for (int e = 0; e < C::E; ++e) av[e] = addmod(av[e], mulmod(b1[e], b2[e], pk), pk.q);
+        for (int e = 0; e < C::E; ++e) {
+          u32 d0 = mulmod(b1[e], b2[e], pk);
+          if (A.dscal) d0 = mul_shoup(d0, ds, dsp, pk.q);
+          av[e] = addmod(av[e], d0, pk.q);
+        }
       } else {
         load_row_step2<L2>(o1, c1 + ((size_t)(A.ne + t) << logN) + lo0, tl);
         load_row_step2<L2>(o2, c2 + ((size_t)(A.ne + t) << logN) + lo0, tl);
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
-          const u32 d1 = reduce64((u64)b1[e] * o2[e] + (u64)o1[e] * b2[e], pk);
+          u32 d1 = reduce64((u64)b1[e] * o2[e] + (u64)o1[e] * b2[e], pk);
+          if (A.dscal) d1 = mul_shoup(d1, ds, dsp, pk.q);
           av[e] = addmod(av[e], d1, pk.q);
         }
       }
@@ -698,7 +735,8 @@ static size_t ks_ws_rows(const LfKsPlan* P, int level) {
 }
 
 // Layout: nsh x [T0 | T1] then batch x [acc | T2 | T3].
-static KsWs carve(const LfCtx* ctx, int level, void* ws, int nsh = 1, bool hoisted = false) {
+static KsWs carve(const LfCtx* ctx, int level, void* ws, int nsh = 1, bool hoisted = false,
+                  int nd = 0) {
   const LfKsPlan* P = ctx->ks;
   const int l1 = level + 1;
   const size_t N = ctx->N;
@@ -710,7 +748,7 @@ static KsWs carve(const LfCtx* ctx, int level, void* ws, int nsh = 1, bool hoist
   p += (size_t)nsh * sh;
   w.acc = p;
   w.T2 = p + 2 * (size_t)l1 * N;
-  w.T3 = w.T2 + 2 * (size_t)P->n_special * N;
+  w.T3 = w.T2 + 2 * (size_t)(P->n_special + nd) * N;     // T3 has 2 nd rows fewer
   w.per_sh = hoisted ? 0 : sh;
   w.per = in;
   return w;
@@ -784,6 +822,7 @@ struct KsCall {
   const u32* glist;
   int b0;                   // first instance of this chunk
   bool ext_out;             // stop after the inner product: out = 2 x ext rows per instance
+  int rescale_nd;           // MUL: fuse a rescale by this many primes into the ModDown (0: none)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -797,7 +836,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   const int l1 = c.level + 1, alpha = P->n_special;
   const size_t N = ctx->N;
   const int nsh = c.hoisted ? 1 : c.batch;
-  const KsWs w = carve(ctx, c.level, ws, nsh, c.hoisted);
+  const int nd = c.op == OP_MUL ? c.rescale_nd : 0;
+  const KsWs w = carve(ctx, c.level, ws, nsh, c.hoisted, nd);
+  const int nt = l1 - nd;                  // output rows per polynomial
   const LfDev dv = ctx->dev();
   const size_t smR = rowpass_smem_bytes<L1, L2>(0);
   const int groups = (1 << L1) / S::LPCR;
@@ -852,6 +893,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.R = P->L + 1 + alpha; A.nbatch = c.batch;
     A.ext_out = c.ext_out ? 1 : 0;
     A.pre = pre ? 1 : 0;
+    A.fuse_nd = nd; A.t2_rows = alpha + nd;
+    A.c1 = c.e0; A.c2 = c.e1; A.c_bs = c.e_bs; A.c_ne = l1;
+    A.pmod = P->pmod;
     if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
     const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
@@ -869,6 +913,10 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.src = w.T2; A.dst = w.T3; A.src_bs = w.per; A.dst_bs = w.per;
     A.ngroups = 2;
     for (int p = 0; p < 2; ++p) {
+      if (nd) {
+        A.g[p] = K.dr[nd - 1][p];
+        continue;
+      }
       A.g[p].B = P->down;
       A.g[p].B.m = l1;                     // prefix of the level-L table
       A.g[p].src_rows = P->iota;
@@ -876,8 +924,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
       A.g[p].src_row0 = p * alpha;
       A.g[p].dst_row0 = p * l1;
     }
-    A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, l1);
-    if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, alpha, s)) return e;
+    A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, nt);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, alpha + nd, s)) return e;
   }
   LF_MARK(4);
   // K_E
@@ -885,11 +933,15 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     ModDownArgs A{};
     A.T3 = w.T3; A.acc = w.acc; A.out = c.out; A.e0 = c.e0; A.e1 = c.e1;
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
-    A.scal = P->rowk + 2; A.sstride = 4; A.nt = l1; A.nacc = l1; A.ne = l1;
+    A.scal = P->rowk + 2; A.sstride = 4; A.nt = nt; A.nacc = l1; A.ne = l1;
+    if (nd) {
+      A.scal = P->pqinv[nd - 1] + (size_t)c.level * P->n_main * 2; A.sstride = 2;
+      A.dscal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)c.level * P->n_main * 2;
+    }
     for (int b = 0; b < c.batch; ++b) A.gs[b] = c.g_of(b);
     A.nbatch = c.batch;
     A.bpc = c.batch >= 2 * LF_BPC ? LF_BPC : 1;
-    dim3 grid(l1 * groups, 1, (c.batch + A.bpc - 1) / A.bpc);
+    dim3 grid(nt * groups, 1, (c.batch + A.bpc - 1) / A.bpc);
     if (c.op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_MUL>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     else if (c.op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_ROT>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
     else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
@@ -1104,6 +1156,23 @@ int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t
   const size_t arow = (size_t)(level + 1) * ctx->N;
   KsCall c{};
   c.level = level; c.batch = batch; c.op = OP_MUL;
+  c.x = ct1 + arow; c.x2 = ct2 + arow; c.x_bs = ct_bstride; c.key = rlk; c.key_bs = 0;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct_bstride;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
+                       const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
+                       size_t out_bstride, int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct1 || !ct2 || !rlk || !out || !workspace) { lf_set_error("lf_hom_mul_rescale: null argument"); return 1; }
+  if (ndrop < 1 || ndrop > 2 || level < ndrop) {
+    lf_set_error("lf_hom_mul_rescale: cannot drop %d primes at level %d", ndrop, level);
+    return 2;
+  }
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop;
   c.x = ct1 + arow; c.x2 = ct2 + arow; c.x_bs = ct_bstride; c.key = rlk; c.key_bs = 0;
   c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct_bstride;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);

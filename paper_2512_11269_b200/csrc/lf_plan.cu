@@ -126,7 +126,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
   }
   Blob blob;
   // identity row list
-  std::vector<u32> iota(n_main > n_sp ? n_main : n_sp);
+  std::vector<u32> iota(n_main > n_sp + 2 ? n_main : n_sp + 2);
   for (size_t i = 0; i < iota.size(); ++i) iota[i] = (u32)i;
   const size_t off_iota = blob.push(iota);
 
@@ -169,6 +169,23 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
       qinv2[((size_t)l * n_main + t) * 2 + 1] = shoupc(v, q);
     }
   const size_t off_qinv2 = blob.push(qinv2);
+  // (P q_l)^-1 and (P q_l q_{l-1})^-1 mod q_t: relinearisation fused with one / two rescales
+  // (mod_down then rescale, poly.py:251-287, as one floor division by P q_l [q_{l-1}])
+  size_t off_pqinv[2];
+  for (int nd = 1; nd <= 2; ++nd) {
+    std::vector<u32> tab((size_t)n_main * n_main * 2, 0);
+    for (int l = nd; l <= L; ++l)
+      for (int t = 0; t <= l - nd; ++t) {
+        const u32 q = primes[t];
+        u32 f = 1;
+        for (int j = 0; j < n_sp; ++j) f = mulm(f, primes[n_main + j] % q, q);
+        for (int u = l - nd + 1; u <= l; ++u) f = mulm(f, primes[u] % q, q);
+        const u32 v = invm(f, q);
+        tab[((size_t)l * n_main + t) * 2] = v;
+        tab[((size_t)l * n_main + t) * 2 + 1] = shoupc(v, q);
+      }
+    off_pqinv[nd - 1] = blob.push(tab);
+  }
 
   // ModDown table: specials -> main 0..L, y-multiplier folds the INTT's N^-1.
   std::vector<int> sp_src, main_all;
@@ -182,7 +199,7 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
     int beta, ext;
     TabRec up[LF_MAXD];
     size_t src_off[LF_MAXD], dst_off[LF_MAXD];
-    TabRec resc, resc2;
+    TabRec resc, resc2, dr[2];
   };
   std::vector<LvRec> lvr(L + 1);
   for (int l = 0; l <= L; ++l) {
@@ -218,6 +235,13 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
       for (int t = 0; t < l - 1; ++t) tgt.push_back(t);
       R.resc2 = build_table(blob, primes, src, tgt, {ninv[l - 1], ninv[l]});
     }
+    for (int nd = 1; nd <= 2 && nd <= l; ++nd) {     // sources in T2 order: specials, then mains
+      std::vector<int> src(sp_src), tgt;
+      std::vector<u32> mult(sp_mult);
+      for (int u = l - nd + 1; u <= l; ++u) { src.push_back(u); mult.push_back(ninv[u]); }
+      for (int t = 0; t <= l - nd; ++t) tgt.push_back(t);
+      R.dr[nd - 1] = build_table(blob, primes, src, tgt, mult);
+    }
   }
 
   void* dmem = nullptr;
@@ -240,6 +264,8 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
   P->pmod = base + off_pmod;
   P->qinv = base + off_qinv;
   P->qinv2 = base + off_qinv2;
+  P->pqinv[0] = base + off_pqinv[0];
+  P->pqinv[1] = base + off_pqinv[1];
   P->down = view(down);
   P->lv.resize(L + 1);
   for (int l = 0; l <= L; ++l) {
@@ -264,6 +290,14 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
         K.resc[p].dst_row0 = p * l;
       }
     }
+    for (int nd = 1; nd <= 2 && nd <= l; ++nd)
+      for (int p = 0; p < 2; ++p) {
+        K.dr[nd - 1][p].B = view(R.dr[nd - 1]);
+        K.dr[nd - 1][p].src_rows = P->iota;
+        K.dr[nd - 1][p].dst_rows = P->iota;
+        K.dr[nd - 1][p].src_row0 = p * (n_sp + nd);
+        K.dr[nd - 1][p].dst_row0 = p * (l + 1 - nd);
+      }
     if (l >= 2) {
       for (int p = 0; p < 2; ++p) {
         K.resc2[p].B = view(R.resc2);

@@ -23,6 +23,8 @@ struct KsLevelPlan {
   BcGroupDev up[LF_MAXD];      // ModUp conversion of digit j (sources G_j, targets ext \ G_j)
   BcGroupDev resc[2];          // rescale at this level: q_level -> q_0..q_{level-1} (b and a)
   BcGroupDev resc2[2];         // double rescale: {q_{level-1}, q_level} -> q_0..q_{level-2}
+  BcGroupDev dr[2][2];         // [nd-1][poly]: ModDown fused with a rescale by nd primes:
+                               // {specials, q_{level-nd+1}..q_level} -> q_0..q_{level-nd}
 };
 
 struct LfKsPlan {
@@ -34,6 +36,7 @@ struct LfKsPlan {
   const u32* pmod;                 // [n_main][2]: P mod q_t and Shoup companion (extended rotations)
   const u32* qinv;                 // [n_main][n_main][2]: q_l^-1 mod q_t and Shoup companion
   const u32* qinv2;                // [n_main][n_main][2]: (q_l q_{l-1})^-1 mod q_t, companion
+  const u32* pqinv[2];             // [n_main][n_main][2]: (P q_l)^-1, (P q_l q_{l-1})^-1 mod q_t
   void* dmem;
 };
 

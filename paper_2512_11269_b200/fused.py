@@ -49,6 +49,21 @@ def hom_mul(params, ct1, ct2, rlk):
     return _pair(out, main_ids(level))
 
 
+def hom_mul_rescale(params, ct1, ct2, rlk, ndrop: int = 1):
+    """hom_mul then `ndrop` rescales (ckks.py:182-194, 220-225), one pipeline: the rescale is
+    folded into the relinearisation's ModDown (lf_hom_mul_rescale).  Returns (b, a) at level
+    ct1.level - ndrop."""
+    ctx = get_context(params)
+    level = ct1.level
+    ws = ctx.ks_workspace(level)
+    c1, c2 = ct_block(ct1), ct_block(ct2)
+    out = torch.empty((2, level + 1 - ndrop, params.N), dtype=torch.int32, device=c1.device)
+    _native.check(_native.lib().lf_hom_mul_rescale(ctx.handle, level, ndrop, dptr(c1), dptr(c2), 0,
+                                                   dptr(rlk.data), dptr(out), 0, 1, dptr(ws),
+                                                   stream_handle()), "lf_hom_mul_rescale")
+    return _pair(out, main_ids(level - ndrop))
+
+
 def rotate(params, ct, g: int, key):
     ctx = get_context(params)
     level = ct.level

@@ -85,7 +85,10 @@ def _upload_rows(raw_u64: np.ndarray):
     from . import _native
     from .context import dptr, stream_handle
     n = raw_u64.size
-    host = torch.from_numpy(np.ascontiguousarray(raw_u64).view(np.int64)).reshape(raw_u64.shape)
+    import warnings
+    with warnings.catch_warnings():          # a read-only view of the blob: only read (pinned copy)
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(np.ascontiguousarray(raw_u64).view(np.int64)).reshape(raw_u64.shape)
     stage = host.pin_memory() if torch.cuda.is_available() else host
     wide = stage.to("cuda", non_blocking=True)
     out = torch.empty(raw_u64.shape, dtype=torch.int32, device="cuda")

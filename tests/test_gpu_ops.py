@@ -235,3 +235,52 @@ def test_double_rescale_equals_two_rescales(B, golden_params, name):
         want = B.rescale(B.rescale(ct, p), p)
         b, a = fused.rescale_multi(p, ct, 2)
         assert np.array_equal(b.numpy(), want.b.numpy()) and np.array_equal(a.numpy(), want.a.numpy())
+
+
+@pytest.mark.parametrize("name", ["small", "desk"])
+def test_mul_rescale_fused_matches_reference(B, golden_params, name):
+    """lf_hom_mul_rescale(ndrop=1) == the reference's rescale(hom_mul(.)) golden vectors."""
+    from paper_2512_11269_b200 import fused
+    p = B.gen_params(**golden_params[name]["kwargs"])
+    meta = load_json(f"ops_{name}.json")
+    sk, pk, rlk, v, w, ct_v, ct_w, rk1, rk3, rkc = _ctx(B, p)
+    low = B.encrypt(B.encode(v, p, level=2), pk, p, np.random.default_rng(2))
+    for key, (x, y) in {"mul_rescale": (ct_v, ct_w), "low_mul_rescale": (low, low)}.items():
+        b, a = fused.hom_mul_rescale(p, x, y, rlk, 1)
+        assert digest(np.stack([b.numpy(), a.numpy()])) == meta["cts"][key]["digest"], key
+
+
+@pytest.mark.parametrize("name", ["desk", "c2"])
+def test_mul_rescale_fused_equals_composition(B, golden_params, name):
+    """ndrop 1 and 2 on full-range random ciphertexts (every residue, so the floor divisions'
+    carries are exercised): equal to hom_mul then ndrop rescales, single and batched."""
+    import torch
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.bootstrap import CtBatch, GpuBackend
+    p = B.gen_params(**golden_params[name]["kwargs"])
+    sk, pk, rlk = B.keygen(p, seed=3)
+    E = B.Domain.EVAL
+    for level in (p.max_level, 2):
+        ids = tuple(range(level + 1))
+        rng = np.random.default_rng(100 + level)
+        rows = lambda: np.stack([rng.integers(0, p.rns_basis[i], p.N, dtype=np.uint64) for i in ids])
+        mk = lambda: B.Ciphertext(B.RnsPolynomial(rows(), E, ids), B.RnsPolynomial(rows(), E, ids),
+                                  p.scale, level)
+        x, y = mk(), mk()
+        prod = B.hom_mul(x, y, rlk, p)
+        for nd in (1, 2):
+            want = prod
+            for _ in range(nd):
+                want = B.rescale(want, p)
+            b, a = fused.hom_mul_rescale(p, x, y, rlk, nd)
+            assert np.array_equal(b.numpy(), want.b.numpy()), (level, nd)
+            assert np.array_equal(a.numpy(), want.a.numpy()), (level, nd)
+        # batch of 3 through the bootstrap backend (one pipeline, shared relinearisation key)
+        be = GpuBackend(p, rlk, None, {})
+        xs, ys = [x, mk(), mk()], [y, mk(), mk()]
+        out = be.mul_rescale2(be.stack(xs), be.stack(ys))
+        for i in range(3):
+            want = B.rescale(B.rescale(B.hom_mul(xs[i], ys[i], rlk, p), p), p)
+            assert np.array_equal(out.data[i, 0].cpu().numpy().astype(np.uint64), want.b.numpy()), (level, i)
+            assert np.array_equal(out.data[i, 1].cpu().numpy().astype(np.uint64), want.a.numpy()), (level, i)
+        torch.cuda.synchronize()
