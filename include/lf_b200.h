@@ -148,6 +148,18 @@ int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct
                     const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
                     size_t out_bstride, void* workspace, void* stream);
 
+/* Permuted-key forms of lf_rotate_hoisted_ext and lf_rotate_batch, bit-identical results.
+ * keys[r] holds the rotation key for gs[r] with every row permuted by the inverse
+ * automorphism: lf_automorph(ctx, pk, key, gs[r]^-1 mod 2N, d * 2 * (L+1+alpha), s).  The
+ * inner product then runs on unpermuted lines (sum_j piece_j * K_j o sigma^-1) and applies
+ * sigma_g once to the two accumulators instead of to every digit's piece. */
+int lf_rotate_hoisted_ext_pk(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                             const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                             size_t out_bstride, void* workspace, void* stream);
+int lf_rotate_batch_pk(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
+                       const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                       size_t out_bstride, void* workspace, void* stream);
+
 /* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,

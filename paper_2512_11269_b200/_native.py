@@ -62,6 +62,9 @@ def _load():
         "lf_rotate_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int,
                                            _u32_host, ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
                                            ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_rotate_batch_pk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int,
+                                              _u32_host, ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
+                                              ctypes.c_void_p, ctypes.c_void_p]),
         "lf_rescale_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                       ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
@@ -75,6 +78,9 @@ def _load():
         "lf_rotate_hoisted_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
                                                  ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
                                                  ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_rotate_hoisted_ext_pk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
+                                                    ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
+                                                    ctypes.c_void_p, ctypes.c_void_p]),
         "lf_moddown_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_moddown_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                           ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),

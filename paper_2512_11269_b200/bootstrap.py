@@ -650,6 +650,26 @@ class GpuBackend:
         self.ck = conj_key
         self.rk = rot_keys
         self._mono = {}
+        self.permuted_keys = True       # rotations through the *_pk entry points (see _pkey)
+        self._pk = {}
+
+    def _pkey(self, steps: int):
+        """Rotation key for `steps` in permuted form (fused.permute_rotation_key), made once and
+        kept resident next to the reference-form key."""
+        from types import SimpleNamespace
+        s = steps % self.params.n
+        k = self._pk.get(s)
+        if k is None:
+            from . import fused
+            k = SimpleNamespace(data=fused.permute_rotation_key(self.params, self.rk[s],
+                                                                galois_element_of(self.N, s)))
+            self._pk[s] = k
+        return k
+
+    def _rot_keys(self, steps):
+        if self.permuted_keys:
+            return [self._pkey(s) for s in steps]
+        return [self.rk[s % self.params.n] for s in steps]
 
     # batches (the two EvalMod evaluations run as one batch of 2 in every kernel)
     def stack(self, cts):
@@ -739,11 +759,12 @@ class GpuBackend:
                          dtype=torch.int32, device="cuda")
         out = torch.empty((n, 2, ext, self.params.N), dtype=torch.int32, device="cuda")
         gs = [galois_element_of(self.params.N, s) for s in steps]
-        keys = [self.rk[s % self.params.n] for s in steps]
+        keys = self._rot_keys(steps)
         karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
         c = ct_block(ct)
-        _native.check(lib.lf_rotate_hoisted_ext(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
-                                                dptr(out), out[0].numel(), dptr(ws), stream_handle()),
+        fn = lib.lf_rotate_hoisted_ext_pk if self.permuted_keys else lib.lf_rotate_hoisted_ext
+        _native.check(fn(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
+                         dptr(out), out[0].numel(), dptr(ws), stream_handle()),
                       "lf_rotate_hoisted_ext")
         return [ExtCt(out[i], ct.scale, level) for i in range(n)]
 
@@ -800,8 +821,8 @@ class GpuBackend:
             src = batch[lo:hi] if batch is not None else torch.stack(
                 [torch.stack([c.b.limbs, c.a.limbs]) for _, c in items[lo:hi]])
             gs = [galois_element_of(self.params.N, st) for _, st in rot]
-            keys = [self.rk[st % self.params.n] for _, st in rot]
-            r = fused.rotate_batch(self.params, level, src, gs, keys)
+            keys = self._rot_keys([st for _, st in rot])
+            r = fused.rotate_batch(self.params, level, src, gs, keys, permuted=self.permuted_keys)
             ids = main_ids(level)
             parts.extend(self.C.Ciphertext(RnsPolynomial(r[j, 0], Domain.EVAL, ids),
                                            RnsPolynomial(r[j, 1], Domain.EVAL, ids), scale, level)
@@ -986,8 +1007,8 @@ class GpuBackend:
             lo, hi = rot_idx[0], rot_idx[-1] + 1
             assert rot_idx == list(range(lo, hi)), "rotated giants must be contiguous"
             gs = [galois_element_of(N, groups[i][0]) for i in rot_idx]
-            keys = [self.rk[groups[i][0] % self.params.n] for i in rot_idx]
-            rot = fused.rotate_batch(self.params, level, inner[lo:hi], gs, keys)
+            keys = self._rot_keys([groups[i][0] for i in rot_idx])
+            rot = fused.rotate_batch(self.params, level, inner[lo:hi], gs, keys, permuted=self.permuted_keys)
             parts.extend(rot[j] for j in range(hi - lo))
         cts = [self.C.Ciphertext(RnsPolynomial(p[0], Domain.EVAL, ids), RnsPolynomial(p[1], Domain.EVAL, ids),
                                  scale, level) for p in parts]

@@ -393,9 +393,14 @@ struct KsInnerArgs {
 #ifndef LF_KSI_MINB
 #define LF_KSI_MINB 2
 #endif
-template <int L1, int L2, bool GALOIS, int XMODE>
+// GMODE 0: no automorphism; 1: sigma_g applied to every digit's piece line before the MAC;
+// 2: permuted keys (keys stored as K o sigma_g^-1, lf_permute_rotation_key): the MAC runs in
+//    the source frame on unpermuted lines, and only the two accumulators are permuted at the end.
+template <int L1, int L2, int GMODE, int XMODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR, LF_KSI_MINB)
 k_ks_inner(KsInnerArgs A, LfDev dv) {
+  constexpr bool GALOIS = GMODE != 0;
+  constexpr bool KP = GMODE == 2;
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int M2 = C::M;
@@ -431,9 +436,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   // the two key rows): issued one digit ahead so the loads at the top of the next iteration hit
   // L1 instead of exposing the full HBM/L2 latency to the first butterfly.
   const int own_j = is_main ? t % A.d : -1;
+  const int hk = KP ? hs : hi;                                // line of the key rows
   auto prefetch_digit = [&](int j) {
     if (j >= A.beta) return;
-    const size_t lo = ((size_t)hi << L2) + (size_t)tl * C::E;
+    const size_t lo = ((size_t)hk << L2) + (size_t)tl * C::E;
     if (j != own_j || A.pre)
       prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
     prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
@@ -457,7 +463,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     if (A.pre) {
       // finished piece: load the source line, permute inside it (sigma_g) through smem
       load_row_step2<L2>(pc, A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2), tl);
-      if (GALOIS) {
+      if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
         for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
@@ -476,7 +482,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e) {
         const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-        const u32 src = GALOIS ? auto_src_index(pos, gal, logN) : pos;
+        const u32 src = KP ? ((u32)hs << L2) + tl * C::E + e : GALOIS ? auto_src_index(pos, gal, logN) : pos;
         u32 v = xr[src];
         if (XMODE == 1) v = mulmod(v, xr2[src], pk);
         pc[e] = mul_shoup_lazy(v, s, sp, pk.q);
@@ -486,7 +492,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       load_row_step2<L2>(pc, tr, tl);
       fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
                         tl, addr, SyncWarp{});
-      if (GALOIS) {
+      if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
         for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
@@ -506,10 +512,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       // key rows are loaded only now (L1-prefetched one digit ahead): keeping them live across
       // the row NTT would push the kernel past 128 registers and spill the twiddle addresses
       u32 kv[C::E];
-      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hk << L2), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kv[e];
-      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hi << L2), tl);
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hk << L2), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kv[e];
     }
@@ -517,8 +523,32 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   u32 rb[C::E], ra[C::E];
 #pragma unroll
   for (int e = 0; e < C::E; ++e) { rb[e] = reduce64(accb[e], pk); ra[e] = reduce64(acca[e], pk); }
+  if (KP) {
+    // source frame -> output line: + P * b (unpermuted) first, then sigma_g on both accumulators
+    if (A.ext_out && is_main) {
+      const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
+      u32 bv[C::E];
+      load_row_step2<L2>(bv, A.eb + ((size_t)t << logN) + ((size_t)hs << L2), tl);
+#pragma unroll
+      for (int e = 0; e < C::E; ++e) rb[e] = addmod(rb[e], mul_shoup(bv[e], pm, pmp, pk.q), pk.q);
+    }
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = rb[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e)
+      rb[e] = perm_buf[auto_src_index(((u32)hi << L2) + tl * C::E + e, gal, logN) & (M2 - 1)];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = ra[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e)
+      ra[e] = perm_buf[auto_src_index(((u32)hi << L2) + tl * C::E + e, gal, logN) & (M2 - 1)];
+    __syncwarp();
+  }
   if (A.ext_out) {
-    if (is_main) {      // + P * sigma_g(b): the b part of the rotation before the division by P
+    if (is_main && !KP) {   // + P * sigma_g(b): the b part of the rotation before the division by P
       const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
       const u32* br = A.eb + ((size_t)t << logN);
 #pragma unroll
@@ -823,6 +853,7 @@ struct KsCall {
   int b0;                   // first instance of this chunk
   bool ext_out;             // stop after the inner product: out = 2 x ext rows per instance
   int rescale_nd;           // MUL: fuse a rescale by this many primes into the ModDown (0: none)
+  bool kperm;               // ROT: keys in permuted form (lf_permute_rotation_key)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -900,9 +931,10 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
     const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
     dim3 grid(K.ext * groups * c.batch);
-    if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, true, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, true, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
-    else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, false, 1>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 1>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
-    else { lf_smem_optin(k_ks_inner<L1, L2, false, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, false, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    if (c.op == OP_ROT && c.kperm) { lf_smem_optin(k_ks_inner<L1, L2, 2, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 2, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    else if (c.op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, 1, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 1, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    else if (c.op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, 0, 1>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 0, 1>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
+    else { lf_smem_optin(k_ks_inner<L1, L2, 0, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 0, 0>, dim3(grid), dim3(S::TRR), smC, s, 1, A, dv)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(3);
@@ -1240,9 +1272,9 @@ int lf_rotate_hoisted(const lf_ctx* ctx, int level, const uint32_t* ct, int n_ro
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
 }
 
-int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
-                    const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
-                    size_t out_bstride, void* workspace, void* stream) {
+static int rotate_batch_impl(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride,
+                             int n, const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                             size_t out_bstride, void* workspace, void* stream, bool kperm) {
   if (int e = ks_check(ctx, level)) return e;
   if (!cts || !gs || !keys || !out || !workspace || n < 1) {
     lf_set_error("lf_rotate_batch: bad argument");
@@ -1255,8 +1287,22 @@ int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct
   c.level = level; c.batch = n; c.op = OP_ROT; c.hoisted = false;
   c.x = cts + arow; c.x2 = c.x; c.x_bs = ct_bstride; c.keylist = keys;
   c.out = out; c.out_bs = out_bstride; c.e0 = cts; c.e1 = nullptr; c.e_bs = ct_bstride;
-  c.glist = gs;
+  c.glist = gs; c.kperm = kperm;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_rotate_batch(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
+                    const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                    size_t out_bstride, void* workspace, void* stream) {
+  return rotate_batch_impl(ctx, level, cts, ct_bstride, n, gs, keys, out, out_bstride, workspace,
+                           stream, false);
+}
+
+int lf_rotate_batch_pk(const lf_ctx* ctx, int level, const uint32_t* cts, size_t ct_bstride, int n,
+                       const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
+                       size_t out_bstride, void* workspace, void* stream) {
+  return rotate_batch_impl(ctx, level, cts, ct_bstride, n, gs, keys, out, out_bstride, workspace,
+                           stream, true);
 }
 
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
@@ -1287,9 +1333,9 @@ int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct
   return 0;
 }
 
-int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
-                          const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
-                          size_t out_bstride, void* workspace, void* stream) {
+static int rotate_hoisted_ext_impl(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                                   const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                                   size_t out_bstride, void* workspace, void* stream, bool kperm) {
   if (int e = ks_check(ctx, level)) return e;
   if (!ct || !gs || !keys || !out_ext || !workspace || n_rot < 1) {
     lf_set_error("lf_rotate_hoisted_ext: bad argument");
@@ -1302,8 +1348,22 @@ int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int 
   c.level = level; c.batch = n_rot; c.op = OP_ROT; c.hoisted = true; c.ext_out = true;
   c.x = ct + arow; c.x2 = c.x; c.x_bs = 0; c.keylist = keys;
   c.out = out_ext; c.out_bs = out_bstride; c.e0 = ct; c.e1 = nullptr; c.e_bs = 0;
-  c.glist = gs;
+  c.glist = gs; c.kperm = kperm;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                          const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                          size_t out_bstride, void* workspace, void* stream) {
+  return rotate_hoisted_ext_impl(ctx, level, ct, n_rot, gs, keys, out_ext, out_bstride, workspace,
+                                 stream, false);
+}
+
+int lf_rotate_hoisted_ext_pk(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot,
+                             const uint32_t* gs, const uint32_t* const* keys, uint32_t* out_ext,
+                             size_t out_bstride, void* workspace, void* stream) {
+  return rotate_hoisted_ext_impl(ctx, level, ct, n_rot, gs, keys, out_ext, out_bstride, workspace,
+                                 stream, true);
 }
 
 size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch) {

@@ -93,8 +93,22 @@ def rotate_hoisted(params, ct, gs, keys):
     return [_pair(out[r], main_ids(level)) for r in range(n)]
 
 
-def rotate_batch(params, level: int, cts: torch.Tensor, gs, keys):
-    """cts: (n, 2, level+1, N) -> n rotations with their own Galois elements and keys."""
+def permute_rotation_key(params, key, g: int) -> torch.Tensor:
+    """The permuted form of a rotation key for Galois element g (every row composed with
+    sigma_g^-1, lf_automorph by g^-1 mod 2N), as the *_pk rotation entry points take it."""
+    ctx = get_context(params)
+    ginv = pow(int(g), -1, 2 * params.N)
+    src = key.data
+    out = torch.empty_like(src)
+    nrows = src.numel() // params.N
+    _native.check(_native.lib().lf_automorph(ctx.handle, dptr(out), dptr(src), ginv, nrows, stream_handle()),
+                  "lf_automorph")
+    return out
+
+
+def rotate_batch(params, level: int, cts: torch.Tensor, gs, keys, permuted: bool = False):
+    """cts: (n, 2, level+1, N) -> n rotations with their own Galois elements and keys
+    (permuted=True: keys in permute_rotation_key form, lf_rotate_batch_pk)."""
     import ctypes
     ctx = get_context(params)
     n = cts.shape[0]
@@ -102,8 +116,9 @@ def rotate_batch(params, level: int, cts: torch.Tensor, gs, keys):
     ws = ctx.ks_workspace(level, min(n, 64))
     out = torch.empty_like(cts)
     karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
-    _native.check(lib.lf_rotate_batch(ctx.handle, level, dptr(cts), cts[0].numel(), n, _native.u32_array(gs),
-                                      karr, dptr(out), out[0].numel(), dptr(ws), stream_handle()),
+    fn = lib.lf_rotate_batch_pk if permuted else lib.lf_rotate_batch
+    _native.check(fn(ctx.handle, level, dptr(cts), cts[0].numel(), n, _native.u32_array(gs),
+                     karr, dptr(out), out[0].numel(), dptr(ws), stream_handle()),
                   "lf_rotate_batch")
     return out
 

@@ -51,6 +51,7 @@ def test_modraise_matches_oracle(env):
 
 
 def test_hoisted_ext_and_moddown_match_oracle(env):
+    import torch
     B, O, p, P, sk, rlk, ko, rk, rko, steps, ct, cto = env
     from oracle.boot_backend import OracleBackend
     from paper_2512_11269_b200 import bootstrap as BT
@@ -58,6 +59,10 @@ def test_hoisted_ext_and_moddown_match_oracle(env):
     bo = OracleBackend(P, ko.rlk, None, rko)
     got = be.rotate_hoisted_ext(ct, steps)
     want = bo.rotate_hoisted_ext(cto, steps)
+    be.permuted_keys = False                 # reference-form keys: the same residues
+    for g, r in zip(got, be.rotate_hoisted_ext(ct, steps)):
+        assert torch.equal(g.data, r.data)
+    be.permuted_keys = True
     for g, w in zip(got, want):
         assert np.array_equal(g.data[0].cpu().numpy().view(np.uint32), w.b.rows.astype(np.uint32))
         assert np.array_equal(g.data[1].cpu().numpy().view(np.uint32), w.a.rows.astype(np.uint32))
@@ -103,10 +108,15 @@ def test_rotate_batch_equals_separate_rotations(env, cfg):
     cts = [B.encrypt(B.encode(np.random.default_rng(i).uniform(-1, 1, p.n), p, level=level), pk, p,
                      np.random.default_rng(50 + i)) for i in range(3)]
     blk = torch.stack([torch.stack([c.b.limbs, c.a.limbs]) for c in cts])
-    out = fused.rotate_batch(p, level, blk, [galois_element(p.N, s) for s in steps], [rk[s] for s in steps])
+    gs = [galois_element(p.N, s) for s in steps]
+    out = fused.rotate_batch(p, level, blk, gs, [rk[s] for s in steps])
     for i, (c, s) in enumerate(zip(cts, steps)):
         want = B.hom_rotate(c, s, rk[s], p)
         assert torch.equal(out[i, 0], want.b.limbs) and torch.equal(out[i, 1], want.a.limbs)
+    # permuted-key form (lf_rotate_batch_pk): bit-identical
+    from types import SimpleNamespace
+    pks = [SimpleNamespace(data=fused.permute_rotation_key(p, rk[s], g)) for s, g in zip(steps, gs)]
+    assert torch.equal(fused.rotate_batch(p, level, blk, gs, pks, permuted=True), out)
 
 
 def test_ptmac_and_lincomb_equal_unfused(env):
