@@ -69,3 +69,14 @@ LF_DEV u32 auto_src_index(u32 i, u32 g, int logN) {
   u32 e = ((2u * r + 1u) * g) & two_n_mask;
   return brev_bits((e - 1u) >> 1, logN);
 }
+
+// For a line-local gather through a bit-reversed staging buffer (element k of a line of 2^lb
+// stored at brev_lb(k)): the slot of auto_src_index(i) & (2^lb - 1), i.e. its bit reversal,
+// which is the top lb bits of the pre-reversal index.  Reads of a warp then hit 32 distinct
+// banks (the map is affine in the bit-reversed domain with an odd multiplier).
+LF_DEV u32 auto_src_slot_brev(u32 i, u32 g, int logN, int lb) {
+  u32 r = brev_bits(i, logN);
+  u32 two_n_mask = (2u << logN) - 1u;
+  u32 e = ((2u * r + 1u) * g) & two_n_mask;
+  return ((e - 1u) >> 1) >> (logN - lb);
+}

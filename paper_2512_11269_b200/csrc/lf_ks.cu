@@ -446,8 +446,9 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
   };
   lf_pdl_trigger();
-  stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
-                       threadIdx.x, blockDim.x);
+  if (!A.pre)           // finished pieces need no row NTT here
+    stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
+                         threadIdx.x, blockDim.x);
   lf_pdl_wait();
   prefetch_digit(0);
   cp_async_wait_all();
@@ -466,12 +467,12 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
-        for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
+        for (int e = 0; e < C::E; ++e) perm_buf[brev_bits(tl * C::E + e, L2)] = pc[e];
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-          pc[e] = perm_buf[auto_src_index(pos, gal, logN) & (M2 - 1)];
+          pc[e] = perm_buf[auto_src_slot_brev(pos, gal, logN, L2)];
         }
       }
     } else if (j == own_j) {
@@ -495,12 +496,12 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
-        for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = pc[e];
+        for (int e = 0; e < C::E; ++e) perm_buf[brev_bits(tl * C::E + e, L2)] = pc[e];
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-          pc[e] = perm_buf[auto_src_index(pos, gal, logN) & (M2 - 1)];
+          pc[e] = perm_buf[auto_src_slot_brev(pos, gal, logN, L2)];
         }
       }
     }
@@ -533,18 +534,18 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       for (int e = 0; e < C::E; ++e) rb[e] = addmod(rb[e], mul_shoup(bv[e], pm, pmp, pk.q), pk.q);
     }
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = rb[e];
+    for (int e = 0; e < C::E; ++e) perm_buf[brev_bits(tl * C::E + e, L2)] = rb[e];
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < C::E; ++e)
-      rb[e] = perm_buf[auto_src_index(((u32)hi << L2) + tl * C::E + e, gal, logN) & (M2 - 1)];
+      rb[e] = perm_buf[auto_src_slot_brev(((u32)hi << L2) + tl * C::E + e, gal, logN, L2)];
     __syncwarp();
 #pragma unroll
-    for (int e = 0; e < C::E; ++e) perm_buf[tl * C::E + e] = ra[e];
+    for (int e = 0; e < C::E; ++e) perm_buf[brev_bits(tl * C::E + e, L2)] = ra[e];
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < C::E; ++e)
-      ra[e] = perm_buf[auto_src_index(((u32)hi << L2) + tl * C::E + e, gal, logN) & (M2 - 1)];
+      ra[e] = perm_buf[auto_src_slot_brev(((u32)hi << L2) + tl * C::E + e, gal, logN, L2)];
     __syncwarp();
   }
   if (A.ext_out) {
