@@ -92,7 +92,7 @@ if "--graph" in sys.argv:
         bt.marks = []
     with torch.cuda.graph(g):
         gout = bt.bootstrap(static_in)
-    gmarks, bt.marks = bt.marks, None
+    gmarks, bt.marks = getattr(bt, "marks", None), None
     g.replay()
     torch.cuda.synchronize()
     dg = B.decrypt(gout, sk, p)
