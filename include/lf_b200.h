@@ -160,6 +160,18 @@ int lf_rotate_batch_pk(const lf_ctx* ctx, int level, const uint32_t* cts, size_t
                        const uint32_t* gs, const uint32_t* const* keys, uint32_t* out,
                        size_t out_bstride, void* workspace, void* stream);
 
+/* One BSGS linear-transform inner sum over the extended basis (hoisted ModDown):
+ *   out[k] = P ct * pts[k][0] + sum_r (P sigma_r(ct.b) + <pieces, K_r>, <pieces, K_r>)_sigma * pts[k][1+r]
+ * i.e. lf_rotate_hoisted_ext_pk of the n_rot rotations (gs, permuted keys) followed by
+ * lf_ptmac_rows for each of the n_giant giant steps, without materialising the rotated
+ * ciphertexts.  pts: HOST array [n_giant][n_rot + 1] of device pointers to extended-basis
+ * plaintexts (level+1+alpha rows, eval domain); NULL where a giant step has no diagonal.
+ * out: n_giant x 2 x (level+1+alpha) rows.  Limits: n_rot <= 32, n_giant <= 4.
+ * Workspace: lf_rotate_hoisted_workspace_bytes(ctx, level, 1). */
+int lf_bsgs_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot, const uint32_t* gs,
+                const uint32_t* const* keys, int n_giant, const uint32_t* const* pts, uint32_t* out,
+                void* workspace, void* stream);
+
 /* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,

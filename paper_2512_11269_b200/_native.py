@@ -81,6 +81,10 @@ def _load():
         "lf_rotate_hoisted_ext_pk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
                                                     ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_size_t,
                                                     ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_bsgs_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,
+                                       ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_void_p,
+                                       ctypes.c_void_p]),
         "lf_moddown_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_moddown_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                           ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),

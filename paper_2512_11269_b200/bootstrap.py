@@ -372,6 +372,18 @@ class Bootstrapper:
         l = ct.level
         S_p = Fraction(S_p)
         lazy = self.cfg.lazy_moddown and hasattr(be, "rotate_hoisted_ext")
+        if lazy and hasattr(be, "bsgs_fused_ext"):
+            # the backend fuses the baby rotations with the giant-step plaintext sums
+            groups = []
+            for k in sorted(plan.giants, key=lambda k: (k != 0, k)):
+                terms = plan.giants[k]
+                pairs = [(b, self._pt((tag, k, b // plan.unit, True), terms[b // plan.unit] * const, l,
+                                      S_p, ext=True))
+                         for b in plan.baby if b // plan.unit in terms]
+                groups.append(((k * plan.g * plan.unit) % self.n, pairs))
+            acc = be.bsgs_fused_ext(ct, groups)
+            if acc is not None:
+                return be.rescale2(acc) if nres == 2 else be.rescale(acc)
         if lazy:
             nz = [b for b in plan.baby if b % self.n]
             ext = dict(zip(nz, be.rotate_hoisted_ext(ct, nz))) if nz else {}
@@ -767,6 +779,65 @@ class GpuBackend:
                          dptr(out), out[0].numel(), dptr(ws), stream_handle()),
                       "lf_rotate_hoisted_ext")
         return [ExtCt(out[i], ct.scale, level) for i in range(n)]
+
+    def bsgs_fused_ext(self, ct, groups):
+        """groups: [(giant shift, [(baby step, extended plaintext)])].  All baby rotations and
+        every giant step's plaintext sum in one lf_bsgs_ext pipeline, then one batched
+        mod_down and the giant rotations (rotate_and_sum).  None when the plan exceeds the
+        kernel's limits (the caller then composes the unfused primitives)."""
+        import ctypes
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .fused import ct_block
+        n = self.params.n
+        rot = sorted({b for _, pairs in groups for b, _ in pairs if b % n})
+        G = len(groups)
+        if not rot or len(rot) > 32 or G > 4 or not self.permuted_keys:
+            return None
+        slot = {b: 1 + i for i, b in enumerate(rot)}
+        ctx = get_context(self.params)
+        lib = _native.lib()
+        level = ct.level
+        ext = level + 1 + self.params.num_special
+        N = self.params.N
+        ptrs = [None] * (G * (len(rot) + 1))
+        pt0 = None
+        for k, (_, pairs) in enumerate(groups):
+            for b, pt in pairs:
+                ptrs[k * (len(rot) + 1) + (slot[b] if b % n else 0)] = pt.poly.limbs.data_ptr()
+                pt0 = pt
+        parr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        keys = self._rot_keys(rot)
+        karr = (ctypes.c_void_p * len(rot))(*[k.data.data_ptr() for k in keys])
+        gs = [galois_element_of(N, b) for b in rot]
+        ws = torch.empty(lib.lf_rotate_hoisted_workspace_bytes(ctx.handle, level, 1) // 4,
+                         dtype=torch.int32, device="cuda")
+        inner = torch.empty((G, 2, ext, N), dtype=torch.int32, device="cuda")
+        _native.check(lib.lf_bsgs_ext(ctx.handle, level, dptr(ct_block(ct)), len(rot), _native.u32_array(gs),
+                                      karr, G, parr, dptr(inner), dptr(ws), stream_handle()), "lf_bsgs_ext")
+        return self._moddown_and_sum(inner, [st for st, _ in groups], ct.scale * pt0.scale, level)
+
+    def _moddown_and_sum(self, inner, shifts, scale, level):
+        """ONE batched mod_down of the giant steps' extended sums (lf_moddown_ext), then the
+        giant rotations and the final sum (rotate_and_sum)."""
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .poly import Domain, RnsPolynomial, main_ids
+        ctx = get_context(self.params)
+        lib = _native.lib()
+        G = inner.shape[0]
+        N = self.params.N
+        out = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
+        ws = torch.empty(lib.lf_moddown_workspace_bytes(ctx.handle, level, G) // 4, dtype=torch.int32,
+                         device="cuda")
+        _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(out),
+                                         out[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
+        ids = main_ids(level)
+        cts = [self.C.Ciphertext(RnsPolynomial(out[i, 0], Domain.EVAL, ids),
+                                 RnsPolynomial(out[i, 1], Domain.EVAL, ids), scale, level) for i in range(G)]
+        return self.rotate_and_sum(list(zip(shifts, cts)), batch=out)
 
     def bsgs_combine_ext(self, groups):
         """Per giant step: sum_b ext_b * pt_{k,b} over the extended basis (lf_ptmac_rows) into one

@@ -601,6 +601,150 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 }
 
 // ---------------------------------------------------------------------------------------
+// K_C fused with the giant-step plaintext sums of a BSGS linear transform (hoisted ModDown):
+// one CTA owns a few lines of one extended-basis row and runs EVERY baby rotation for them,
+//   rot_r = sigma_r(P b + sum_j piece_j * K'_rj)  (permuted keys K' = K o sigma^-1, source frame)
+// and accumulates out_k += rot_r * pt_{k,r} for every giant k in registers.  The rotated
+// extended ciphertexts never reach memory; only the giant sums (ngiant x 2 x ext rows) do.
+// Bit-identical to lf_rotate_hoisted_ext + lf_ptmac_rows (exact modular sums, any order).
+#define LF_BSGS_GMAX 4
+#define LF_BSGS_RMAX 32
+struct BsgsExtArgs {
+  const u32* T1;                 // beta x ext finished eval-domain pieces (k_pieces, natural)
+  const u32* ct;                 // b rows then a rows (level+1 each)
+  const u32* pmod;               // [n_main][2]: P mod q_t, Shoup companion
+  u32* out;                      // ngiant x 2 x ext rows
+  int level, L, alpha, beta, R, ext, nrot, ngiant;
+  const u32* keyp[LF_BSGS_RMAX];                 // permuted key of rotation r
+  u32 gs[LF_BSGS_RMAX];
+  const u32* pt[LF_BSGS_GMAX][LF_BSGS_RMAX + 1]; // [giant][0: identity baby, 1 + r: rotation r]
+};
+
+template <int L1, int L2>
+struct BsgsShape {
+  static constexpr int M2 = 1 << L2;              // line length
+  static constexpr int TPL = M2 / 4;              // threads per line (4 consecutive words each)
+  static constexpr int LINES0 = 256 / TPL;
+  static constexpr int LINES = LINES0 < (1 << L1) ? LINES0 : (1 << L1);
+  static constexpr int THREADS = LINES * TPL;
+};
+
+template <int L1, int L2, int G>
+__global__ void __launch_bounds__(BsgsShape<L1, L2>::THREADS)
+k_bsgs_ext(BsgsExtArgs A, LfDev dv) {
+  using S = BsgsShape<L1, L2>;
+  constexpr int logN = L1 + L2;
+  constexpr int M2 = S::M2;
+  __shared__ u32 buf[S::LINES * M2];
+  const int ln = threadIdx.x / S::TPL, tid = threadIdx.x % S::TPL;
+  constexpr int CPR = (1 << L1) / S::LINES;       // CTAs per row
+  const int t = blockIdx.x / CPR;
+  const int hi = (blockIdx.x % CPR) * S::LINES + ln;
+  const int l = A.level;
+  const bool is_main = t <= l;
+  const int pi = is_main ? t : A.L + 1 + (t - l - 1);
+  const PrimeK pk = dv.pk[pi];
+  const int ext = A.ext;
+  u32* lb = buf + ln * M2;
+  const int e0 = tid * 4;
+  u32 pm = 0, pmp = 0;
+  if (is_main) { pm = A.pmod[2 * t]; pmp = A.pmod[2 * t + 1]; }
+  lf_pdl_trigger();
+  lf_pdl_wait();
+
+  u32 ob[G][4], oa[G][4];
+#pragma unroll
+  for (int k = 0; k < G; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { ob[k][e] = 0; oa[k][e] = 0; }
+
+  // identity baby: P * ct on the main rows (its special rows are zero)
+  if (is_main) {
+    const uint4 vb = *reinterpret_cast<const uint4*>(A.ct + ((size_t)t << logN) + ((size_t)hi << L2) + e0);
+    const uint4 va = *reinterpret_cast<const uint4*>(A.ct + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2) + e0);
+    const u32 xb[4] = {vb.x, vb.y, vb.z, vb.w}, xa[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const u32* p = A.pt[k][0];
+      if (!p) continue;
+      const uint4 pv = *reinterpret_cast<const uint4*>(p + ((size_t)t << logN) + ((size_t)hi << L2) + e0);
+      const u32 pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const u32 w = mul_shoup(pw[e], pm, pmp, pk.q);           // P * pt
+        ob[k][e] = addmod(ob[k][e], mulmod(xb[e], w, pk), pk.q);
+        oa[k][e] = addmod(oa[k][e], mulmod(xa[e], w, pk), pk.q);
+      }
+    }
+  }
+
+#pragma unroll 1
+  for (int r = 0; r < A.nrot; ++r) {
+    const u32 g = A.gs[r];
+    const int hs = (int)(auto_src_index((u32)hi << L2, g, logN) >> L2);
+    const size_t src = ((size_t)hs << L2) + e0;
+    const u32* key = A.keyp[r];
+    u64 ab[4] = {0, 0, 0, 0}, aa[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int j = 0; j < A.beta; ++j) {
+      const uint4 pc = *reinterpret_cast<const uint4*>(A.T1 + ((size_t)(j * ext + t) << logN) + src);
+      const uint4 kb = *reinterpret_cast<const uint4*>(key + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + src);
+      const uint4 ka = *reinterpret_cast<const uint4*>(key + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + src);
+      ab[0] += (u64)pc.x * kb.x; ab[1] += (u64)pc.y * kb.y; ab[2] += (u64)pc.z * kb.z; ab[3] += (u64)pc.w * kb.w;
+      aa[0] += (u64)pc.x * ka.x; aa[1] += (u64)pc.y * ka.y; aa[2] += (u64)pc.z * ka.z; aa[3] += (u64)pc.w * ka.w;
+      if (A.beta > 15 && (j & 15) == 15) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { ab[e] = reduce64(ab[e], pk); aa[e] = reduce64(aa[e], pk); }
+      }
+    }
+    u32 rb[4], ra[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { rb[e] = reduce64(ab[e], pk); ra[e] = reduce64(aa[e], pk); }
+    if (is_main) {          // + P * b, then sigma_r (source frame -> output line)
+      const uint4 bv = *reinterpret_cast<const uint4*>(A.ct + ((size_t)t << logN) + src);
+      const u32 bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rb[e] = addmod(rb[e], mul_shoup(bw[e], pm, pmp, pk.q), pk.q);
+    }
+    u32 sl[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sl[e] = auto_src_slot_brev(((u32)hi << L2) + e0 + e, g, logN, L2);
+    __syncthreads();                       // previous rotation's reads of buf are done
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lb[brev_bits(e0 + e, L2)] = rb[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) rb[e] = lb[sl[e]];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lb[brev_bits(e0 + e, L2)] = ra[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ra[e] = lb[sl[e]];
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const u32* p = A.pt[k][1 + r];
+      if (!p) continue;
+      const uint4 pv = *reinterpret_cast<const uint4*>(p + ((size_t)t << logN) + ((size_t)hi << L2) + e0);
+      const u32 pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ob[k][e] = addmod(ob[k][e], mulmod(rb[e], pw[e], pk), pk.q);
+        oa[k][e] = addmod(oa[k][e], mulmod(ra[e], pw[e], pk), pk.q);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    if (k >= A.ngiant) break;
+    u32* ob_ = A.out + ((size_t)((k * 2 + 0) * ext + t) << logN) + ((size_t)hi << L2) + e0;
+    u32* oa_ = A.out + ((size_t)((k * 2 + 1) * ext + t) << logN) + ((size_t)hi << L2) + e0;
+    *reinterpret_cast<uint4*>(ob_) = make_uint4(ob[k][0], ob[k][1], ob[k][2], ob[k][3]);
+    *reinterpret_cast<uint4*>(oa_) = make_uint4(oa[k][0], oa[k][1], oa[k][2], oa[k][3]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // K_E: row pass of the NTT of the converted rows, (acc - conv) * scalar, epilogue.
 enum { EPI_KS = 0, EPI_MUL = 1, EPI_ROT = 2 };
 struct ModDownArgs {
@@ -855,6 +999,7 @@ struct KsCall {
   bool ext_out;             // stop after the inner product: out = 2 x ext rows per instance
   int rescale_nd;           // MUL: fuse a rescale by this many primes into the ModDown (0: none)
   bool kperm;               // ROT: keys in permuted form (lf_permute_rotation_key)
+  const BsgsExtArgs* bsgs;  // hoisted ROT: K_C fused with the giant-step sums (k_bsgs_ext)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -907,7 +1052,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   }
   // hoisted batch: finish the NTT of every piece ONCE (in place, natural layout); each rotation's
   // inner product then only permutes and multiplies (no per-rotation row NTT)
-  const bool pre = c.hoisted && c.batch > 1;
+  const bool pre = c.hoisted && (c.batch > 1 || c.bsgs);
   if (pre) {
     dim3 grid(K.beta * K.ext * groups);
     lf_smem_optin(k_pieces<L1, L2>, smR);
@@ -916,6 +1061,21 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     LF_CHECK_LAUNCH();
   }
   LF_MARK(2);
+  if (c.bsgs) {
+    using SB = BsgsShape<L1, L2>;
+    BsgsExtArgs A = *c.bsgs;
+    A.T1 = w.T1; A.pmod = P->pmod; A.level = c.level; A.L = P->L; A.alpha = alpha;
+    A.beta = K.beta; A.R = P->L + 1 + alpha; A.ext = K.ext;
+    dim3 grid(K.ext * ((1 << L1) / SB::LINES));
+    switch (A.ngiant) {
+#define LF_BG(GG) case GG: LF_LAUNCH_CHECK(lf_launch(k_bsgs_ext<L1, L2, GG>, grid, dim3(SB::THREADS), 0, s, 1, A, dv)); break;
+      LF_BG(1) LF_BG(2) LF_BG(3) LF_BG(4)
+#undef LF_BG
+      default: lf_set_error("bsgs: %d giant steps (max %d)", A.ngiant, LF_BSGS_GMAX); return 2;
+    }
+    LF_CHECK_LAUNCH();
+    return 0;
+  }
   // K_C
   {
     KsInnerArgs A{};
@@ -1365,6 +1525,32 @@ int lf_rotate_hoisted_ext_pk(const lf_ctx* ctx, int level, const uint32_t* ct, i
                              size_t out_bstride, void* workspace, void* stream) {
   return rotate_hoisted_ext_impl(ctx, level, ct, n_rot, gs, keys, out_ext, out_bstride, workspace,
                                  stream, true);
+}
+
+int lf_bsgs_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot, const uint32_t* gs,
+                const uint32_t* const* keys, int n_giant, const uint32_t* const* pts, uint32_t* out,
+                void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct || !gs || !keys || !pts || !out || !workspace || n_rot < 1 || n_rot > LF_BSGS_RMAX ||
+      n_giant < 1 || n_giant > LF_BSGS_GMAX) {
+    lf_set_error("lf_bsgs_ext: bad argument (n_rot %d <= %d, n_giant %d <= %d)", n_rot, LF_BSGS_RMAX,
+                 n_giant, LF_BSGS_GMAX);
+    return 1;
+  }
+  for (int r = 0; r < n_rot; ++r)
+    if (!(gs[r] & 1) || !keys[r]) { lf_set_error("lf_bsgs_ext: rotation %d: bad key or even galois element", r); return 2; }
+  BsgsExtArgs B{};
+  B.ct = ct; B.out = out; B.nrot = n_rot; B.ngiant = n_giant;
+  for (int r = 0; r < n_rot; ++r) { B.keyp[r] = keys[r]; B.gs[r] = gs[r] & ((2u << ctx->logN) - 1); }
+  for (int k = 0; k < n_giant; ++k)
+    for (int r = 0; r <= n_rot; ++r) B.pt[k][r] = pts[(size_t)k * (n_rot + 1) + r];
+  const size_t arow = (size_t)(level + 1) * ctx->N;
+  KsCall c{};
+  c.level = level; c.batch = n_rot; c.op = OP_ROT; c.hoisted = true; c.ext_out = true; c.kperm = true;
+  c.x = ct + arow; c.x2 = c.x; c.x_bs = 0; c.keylist = keys;
+  c.out = out; c.out_bs = 0; c.e0 = ct; c.e1 = nullptr; c.e_bs = 0;
+  c.glist = gs; c.bsgs = &B;
+  return run_ks_chunk(ctx, c, workspace, (cudaStream_t)stream, nullptr);
 }
 
 size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch) {

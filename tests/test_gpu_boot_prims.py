@@ -78,6 +78,13 @@ def test_hoisted_ext_and_moddown_match_oracle(env):
     w = bo.bsgs_combine_ext(groups_o)
     assert g.scale == w.scale
     assert np.array_equal(g.b.numpy(), w.b.rows) and np.array_equal(g.a.numpy(), w.a.rows)
+    # fused baby rotations + giant sums (lf_bsgs_ext) == hoisted_ext + ptmac_rows composition
+    ext_map = {0: be.extend(ct), **dict(zip(steps, got))}
+    gspec = [(0, [(0, pts[0]), (1, pts[1])]), (3, [(3, pts[1]), (7, pts[2]), (0, pts[2])])]
+    fz = be.bsgs_fused_ext(ct, gspec)
+    un = be.bsgs_combine_ext([(sh, [(ext_map[b], pt) for b, pt in prs]) for sh, prs in gspec])
+    assert fz.scale == un.scale
+    assert torch.equal(fz.b.limbs, un.b.limbs) and torch.equal(fz.a.limbs, un.a.limbs)
     # and P*ct extends exactly: mod_down(P*ct) == ct
     e = be.extend(ct)
     from paper_2512_11269_b200 import fused  # noqa: F401
