@@ -172,6 +172,33 @@ int lf_bsgs_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int n_rot, con
                 const uint32_t* const* keys, int n_giant, const uint32_t* const* pts, uint32_t* out,
                 void* workspace, void* stream);
 
+/* ---- kernel-plan interpreter (the reference's KernelRunner boundary, codegen.py:346-443) ----
+ * One step of a compiled kernel plan: op i of every lane, one launch.  ops is a DEVICE array of
+ * nops lf_plan_op records; each reads its sources at coefficient n, writes the canonical
+ * result to dst (a register row) and, when store != NULL, to the operand row (the lane op's
+ * store_slot).  Opcodes follow limbir.py:46-56; COPY stages a row (for the NTT/INTT steps,
+ * which run through lf_ntt_fwd / lf_ntt_inv on the step's contiguous register rows). */
+#define LF_POP_ADD 0        /* row_add      poly.py:85   */
+#define LF_POP_SUB 1        /* row_sub      poly.py:89   */
+#define LF_POP_MUL 2        /* row_mul      poly.py:94   */
+#define LF_POP_MULACC 3     /* src0 + src1 * src2 (codegen.py:389-391) */
+#define LF_POP_NEG 4        /* row_neg      poly.py:104  */
+#define LF_POP_SCALARMUL 5  /* row_scalar_mul poly.py:108 */
+#define LF_POP_MODSTEP 6    /* row_modstep  poly.py:112  */
+#define LF_POP_AUTOMORPH 7  /* out[i] = src[perm_g(i)] (ntt.py:108-126) */
+#define LF_POP_BCONV 8      /* exact conversion of k source rows to the lane prime (poly.py:150-178) */
+#define LF_POP_COPY 9
+typedef struct lf_plan_op {
+  int32_t opcode, pidx;          /* LF_POP_*, prime index of the lane */
+  uint32_t scalar, galois;       /* scalar reduced mod the lane prime; galois element (odd) */
+  int32_t nsrc, k, W, pad;       /* sources; BConv: k sources and table words */
+  const uint32_t* const* src;    /* device array of nsrc device row pointers */
+  uint32_t* dst;                 /* register row (may be NULL) */
+  uint32_t* store;               /* operand row to store into, or NULL */
+  const uint32_t* table;         /* BConv table blob (k sources -> 1 target), else NULL */
+} lf_plan_op;
+int lf_plan_step(const lf_ctx* ctx, const lf_plan_op* ops, int nops, void* stream);
+
 /* rescale (ckks.py:220-225, poly.py:284-287): out = 2 x level rows. */
 size_t lf_rescale_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstride,

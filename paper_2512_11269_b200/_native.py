@@ -85,6 +85,7 @@ def _load():
                                        ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_void_p), _u32p, ctypes.c_void_p,
                                        ctypes.c_void_p]),
+        "lf_plan_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
         "lf_moddown_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
         "lf_moddown_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_size_t, _u32p,
                                           ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),

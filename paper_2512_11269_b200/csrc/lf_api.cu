@@ -245,4 +245,9 @@ int lf_mul_compressed(const lf_ctx* ctx, uint32_t* out, const uint32_t* ct, cons
   return lf_launch_mul_compressed(ctx, out, ct, unique, nrows, unique_count, lb, (cudaStream_t)stream);
 }
 
+int lf_plan_step(const lf_ctx* ctx, const lf_plan_op* ops, int nops, void* stream) {
+  if (!ctx || (!ops && nops > 0)) { lf_set_error("lf_plan_step: null argument"); return 1; }
+  return lf_launch_plan_step(ctx, ops, nops, (cudaStream_t)stream);
+}
+
 }  // extern "C"

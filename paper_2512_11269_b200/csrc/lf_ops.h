@@ -22,3 +22,4 @@ int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u3
 int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStream_t s);
 int lf_launch_mul_compressed(const LfCtx* ctx, u32* out, const u32* ct, const u32* uq, int nrows,
                              int ucount, int lb, cudaStream_t s);
+int lf_launch_plan_step(const LfCtx* ctx, const void* ops, int nops, cudaStream_t s);

@@ -14,6 +14,13 @@ The wrappers accept reference objects (CkksParams, Ciphertext, Plaintext, EvalKe
 uint64 numpy rows) and return this package's device-resident objects, which every wrapped
 operator also accepts, so a circuit stays on the GPU between operations.  Reference
 evaluation keys are uploaded once and cached per key object.
+
+The compiled pipeline (pipeline.py / runtime.py Executor) instead executes kernel plans through
+`KernelRunner`; `install_runner(limbforge.runtime)` swaps that class for the B200 runner:
+
+    import limbforge.runtime as rt
+    with dropin.install_runner(rt):
+        result = rt.Executor(compiled, ...).run(...)        # every kernel plan on the GPU
 """
 
 from fractions import Fraction
@@ -103,6 +110,31 @@ class Installed:
     def __exit__(self, *exc):
         self.restore()
         return False
+
+
+class KernelRunner:
+    """Stand-in for `limbforge.codegen.KernelRunner` (codegen.py:346-361) constructed with a
+    reference CkksParams, as `Executor` (runtime.py:188) and the multi-device runner
+    (multidev.py:801) do; runs every plan on the B200 (kernel_runner.KernelRunner)."""
+
+    def __init__(self, params, max_regs: int = 512):
+        from .kernel_runner import KernelRunner as _Gpu
+        self.params = params
+        self._gpu = _Gpu(as_params(params), max_regs)
+
+    def run(self, plan, read_row, write_row):
+        self._gpu.run(plan, read_row, write_row)
+
+
+def install_runner(module) -> Installed:
+    """Replace the `KernelRunner` global of `module` (`limbforge.runtime` or
+    `limbforge.multidev`, which bind it at import: runtime.py:21, multidev.py:29), so the
+    compiled pipeline's kernels run on the B200."""
+    saved = {}
+    if hasattr(module, "KernelRunner"):
+        saved["KernelRunner"] = module.KernelRunner
+        module.KernelRunner = KernelRunner
+    return Installed(module, saved)
 
 
 def install(module) -> Installed:

@@ -47,3 +47,11 @@ def test_reference_params_convert():
     assert conv == own
     assert dropin.as_params(ref_like) is conv          # cached per object
     assert dropin.as_params(own) is own
+
+
+def test_install_runner_swaps_kernel_runner():
+    m = types.ModuleType("fake_runtime")
+    m.KernelRunner = "orig"
+    with dropin.install_runner(m):
+        assert m.KernelRunner is dropin.KernelRunner
+    assert m.KernelRunner == "orig"
