@@ -343,6 +343,65 @@ def batch_sweep(params, level, rlk, dev, batches=(1, 8), steps=5):
     return out
 
 
+def rotation_units(params, level, dev, steps=5):
+    """The other C2 units of SURVEY §8d: one hom_rotate (lf_rotate, batch 1), 32 independent
+    rotations in one pipeline (lf_rotate_batch, keys cycling over steps 1..8) and a hoisted
+    batch of 8 rotations of one ciphertext sharing one ModUp (lf_rotate_hoisted, full
+    semantics incl. ModDown).  Keys and ciphertexts are synthetic uniform rows (cost is
+    data-independent); L2 flushed between timed runs; CUDA events."""
+    import torch
+    from types import SimpleNamespace
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.ntt_host import galois_element
+    l1, N = level + 1, params.N
+    alpha, d = params.num_special, params.ks.d
+    R = params.max_level + 1 + alpha
+    primes = list(params.rns_basis) + list(params.special_basis)
+    g = torch.Generator(device=dev).manual_seed(4242)
+
+    def rows(idx, lead=()):
+        q = torch.tensor([primes[i] for i in idx], dtype=torch.int64, device=dev)[:, None]
+        r = torch.randint(0, 2 ** 62, (*lead, len(idx), N), device=dev, generator=g, dtype=torch.int64)
+        return (r % q).to(torch.int32)
+    kidx = list(range(params.max_level + 1)) + list(range(params.max_level + 1, params.max_level + 1 + alpha))
+    keys = [SimpleNamespace(data=rows(kidx, (d, 2)).contiguous()) for _ in range(8)]
+    gs = [galois_element(N, s) for s in range(1, 9)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def ct_of(t):
+        return SimpleNamespace(b=SimpleNamespace(limbs=t[0]), a=SimpleNamespace(limbs=t[1]), level=level)
+
+    def timed(fn):
+        fn()
+        fn()
+        ms = 0.0
+        for i in range(steps):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        return ms / steps
+    ct1 = rows(list(range(l1)) * 2).view(2, l1, N)
+    one = timed(lambda: fused.rotate(params, ct_of(ct1), gs[0], keys[0]))
+    cts = rows(list(range(l1)) * 2, (32,)).view(32, 2, l1, N)
+    b32 = timed(lambda: fused.rotate_batch(params, level, cts, [gs[i % 8] for i in range(32)],
+                                           [keys[i % 8] for i in range(32)]))
+    h8 = timed(lambda: fused.rotate_hoisted(params, ct_of(ct1), gs, keys))
+    beta = min(d, l1)
+    ext = l1 + alpha
+    h8_bytes = (2 * l1 + 8 * (2 * beta * ext + 2 * l1)) * N * 4
+    rot_bytes = (4 * l1 + 2 * beta * ext) * N * 4
+    return {"hom_rotate_us": one * 1e3, "rotate_batch32_us_per_op": b32 / 32 * 1e3,
+            "hoisted8_us": h8 * 1e3, "hoisted8_us_per_rotation": h8 / 8 * 1e3,
+            "hoisted8_algorithmic_bytes": h8_bytes,
+            "hoisted8_hbm_gbs": h8_bytes / (h8 / 1e3) / 1e9,
+            "rotate_algorithmic_bytes": rot_bytes,
+            "keys": "synthetic uniform rows (8 rotation keys, steps 1..8)"}
+
+
 def ntt_summary(ntt, clocks):
     mhz = (clocks or {}).get("sm_mhz") or 1965
     peak = 32 * 148 * mhz * 1e6                  # IMAD.HI per second (one per butterfly)
@@ -506,6 +565,7 @@ def run_ours(args, rank, world):
 
     ntt = ntt_throughput(params, dev)
     sweep = batch_sweep(params, level, rlk, dev) if rank == 0 else None
+    rot = rotation_units(params, level, dev) if rank == 0 else None
 
     sharded = None
     if world > 1:
@@ -545,6 +605,7 @@ def run_ours(args, rank, world):
             "bootstrap": boot,
             "ntt": ntt_summary(ntt, clocks),
             "batch_sweep": sweep,
+            "rotation": rot,
             "limb_sharded": sharded,
         }
         print(json.dumps(line), flush=True)
