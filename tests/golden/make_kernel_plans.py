@@ -148,6 +148,24 @@ def _execute(name, params, dag, plans, seed, KernelRunner):
     return out
 
 
+def make_program(name, params, text, seed):
+    """Every compiled segment of every function of a program (pipeline.compile_source), each
+    with its own inputs, plans and written-row digests."""
+    from limbforge.codegen import KernelRunner
+    from limbforge.pipeline import compile_source
+    comp = compile_source(text, params)
+    segs = []
+    for fname in sorted(comp.functions):
+        for k, st in enumerate(comp.functions[fname].steps):
+            if not hasattr(st, "schedule"):
+                continue                                   # CallStep
+            sub = _execute(f"{name}:{fname}:{k}", params, st.dag, st.schedule.plans,
+                           seed + len(segs), KernelRunner)
+            segs.append(sub)
+    return {"name": name, "segments": segs,
+            "opcodes": sorted({o for sg in segs for o in sg["opcodes"]})}
+
+
 def main():
     sys.path.insert(0, "/root/reference/pkg/src")
     from limbforge.bench import bsgs64
@@ -162,6 +180,14 @@ def main():
     fx2["gen_params"] = fx["gen_params"]
     fx3 = make_dag("synth_allops_n256", p, synth_dag(p), seed=99)
     fx3["gen_params"] = fx["gen_params"]
+    from limbforge.bench import tinylayer
+    p10 = gen_params(256, 10, d=3, seed=3)
+    fx4 = make_program("tinylayer_n256", p10, tinylayer(p10).text, seed=555)
+    fx4["gen_params"] = {"N": 256, "num_levels": 10, "d": 3, "seed": 3}
+    with open(os.path.join(HERE, "kernel_plans_tinylayer.json"), "w") as f:
+        json.dump(fx4, f)
+    print(fx4["name"], len(fx4["segments"]), "segments,", sum(len(sg["plans"]) for sg in fx4["segments"]),
+          "plans,", sum(len(sg["written"]) for sg in fx4["segments"]), "rows written; opcodes", fx4["opcodes"])
     for fname, f_ in (("kernel_plans_bsgs16.json", fx), ("kernel_plans_polyeval7.json", fx2),
                       ("kernel_plans_synth.json", fx3)):
         with open(os.path.join(HERE, fname), "w") as f:

@@ -1,8 +1,10 @@
 """KernelRunner boundary (reference codegen.py:346-443).
 
-The fixtures hold kernel plans the reference compiler produced for two compiled programs (a
-BSGS mat-vec and a polynomial evaluation at N=256) and a synthetic plan covering every limb
-opcode, plus the digests of every row the reference KernelRunner wrote
+The fixtures hold kernel plans the reference compiler produced for three compiled programs at
+N=256 (a BSGS mat-vec — the rotate-and-sum of BASELINE config 4; a degree-7 polynomial — the
+polynomial activation; and the reference's `tinylayer` — mat-vec, GELU polynomial, mat-vec, the
+transformer-block shape of config 5) and a synthetic plan covering every limb opcode, plus the
+digests of every row the reference KernelRunner wrote
 (tests/golden/make_kernel_plans.py).  CPU: the oracle restatement reproduces them.  GPU: the
 B200 runner (`paper_2512_11269_b200.kernel_runner`) reproduces them with device-resident rows
 and with the reference's host-row callbacks.
@@ -16,12 +18,20 @@ import numpy as np
 import pytest
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-FIXTURES = ["kernel_plans_bsgs16.json", "kernel_plans_polyeval7.json", "kernel_plans_synth.json"]
+FIXTURES = ["kernel_plans_bsgs16.json", "kernel_plans_polyeval7.json", "kernel_plans_synth.json",
+            "kernel_plans_tinylayer.json"]
 
 
 def _load(name):
     with open(os.path.join(GOLD, name)) as f:
         return json.load(f)
+
+
+def _segments(fx):
+    """A fixture is one compiled segment, or a program with several (tinylayer: matvec, GELU
+    polynomial, matvec across three functions)."""
+    for sg in fx.get("segments", [fx]):
+        yield dict(sg, gen_params=fx["gen_params"])
 
 
 def _digest(row) -> str:
@@ -60,14 +70,16 @@ def _check(fx, get_row):
 def test_oracle_runner_matches_reference(name):
     from oracle import lf_oracle as O
     from oracle.kernel_runner import KernelRunner, plan_from_json
-    fx = _load(name)
-    P = O.gen_params(**fx["gen_params"])
-    rows = _inputs(fx, P.prime)
-    store, read, write = _host_store(fx, rows, P.N)
+    fx0 = _load(name)
+    P = O.gen_params(**fx0["gen_params"])
     runner = KernelRunner(P)
-    for pl in fx["plans"]:
-        runner.run(plan_from_json(pl), read, write)
-    _check(fx, lambda l: store[l])
+    for fx in _segments(fx0):
+        rows = _inputs(fx, P.prime)
+        store, read, write = _host_store(fx, rows, P.N)
+        for pl in fx["plans"]:
+            runner.run(plan_from_json(pl), read, write)
+        _check(fx, lambda l: store[l])
+    fx = fx0
     assert set(fx["opcodes"]) <= {"Add", "Sub", "Mul", "MulAcc", "Neg", "ScalarMul", "ModStep",
                                   "Automorph", "NTT", "INTT", "BConv"}
 
@@ -90,11 +102,18 @@ def test_gpu_runner_matches_reference(name, mode):
         pytest.skip("no CUDA device")
     import paper_2512_11269_b200 as B
     from paper_2512_11269_b200.kernel_runner import KernelRunner, plan_from_json
-    fx = _load(name)
-    p = B.gen_params(**fx["gen_params"])
+    fx0 = _load(name)
+    p = B.gen_params(**fx0["gen_params"])
     from paper_2512_11269_b200.poly import prime_for_id
-    rows = _inputs(fx, lambda b: prime_for_id(p, b))
     runner = KernelRunner(p)
+    for fx in _segments(fx0):
+        _gpu_segment(fx, p, runner, mode, lambda b: prime_for_id(p, b))
+
+
+def _gpu_segment(fx, p, runner, mode, prime_of):
+    import torch
+    from paper_2512_11269_b200.kernel_runner import plan_from_json
+    rows = _inputs(fx, prime_of)
     plans = [plan_from_json(pl) for pl in fx["plans"]]
     if mode == "host":                  # the reference Executor's callbacks: uint64 host rows
         store, read, write = _host_store(fx, rows, p.N)
