@@ -57,7 +57,7 @@ def hom_mul_rescale(params, ct1, ct2, rlk, ndrop: int = 1):
     level = ct1.level
     ws = ctx.ks_workspace(level)
     c1, c2 = ct_block(ct1), ct_block(ct2)
-    out = torch.empty((2, level + 1 - ndrop, params.N), dtype=torch.int32, device=c1.device)
+    out = torch.empty((2, max(level + 1 - ndrop, 1), params.N), dtype=torch.int32, device=c1.device)
     _native.check(_native.lib().lf_hom_mul_rescale(ctx.handle, level, ndrop, dptr(c1), dptr(c2), 0,
                                                    dptr(rlk.data), dptr(out), 0, 1, dptr(ws),
                                                    stream_handle()), "lf_hom_mul_rescale")

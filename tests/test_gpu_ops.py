@@ -156,6 +156,17 @@ def test_error_paths(B, golden_params):
     with pytest.raises(ValueError):
         B.make_rotation_key(p, sk, 0, np.random.default_rng(0))
     assert B.hom_rotate(ct, p.n, None, p) is ct
+    # C-ABI argument checks of the fused entry points fail loudly (no silent fallback)
+    from paper_2512_11269_b200 import _native, fused
+    with pytest.raises(_native.NativeError, match="lf_hom_mul_rescale"):
+        fused.hom_mul_rescale(p, ct0, ct0, rlk, 1)           # level 0 cannot drop a prime
+    with pytest.raises(_native.NativeError, match="lf_hom_mul_rescale"):
+        fused.hom_mul_rescale(p, ct, ct, rlk, 3)             # ndrop outside {1, 2}
+    lib = _native.lib()
+    from paper_2512_11269_b200.context import get_context
+    import ctypes
+    rc = lib.lf_bsgs_ext(get_context(p).handle, ct.level, None, 0, None, None, 0, None, None, None, None)
+    assert rc != 0 and b"lf_bsgs_ext" in lib.lf_last_error()
 
 
 @pytest.mark.parametrize("level", [35, 20])
