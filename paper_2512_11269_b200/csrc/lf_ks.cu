@@ -65,9 +65,9 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   const int pi = pbase + row % rpp;
   const PrimeK pk = dv.pk[pi];
   uint2* tws = reinterpret_cast<uint2*>(sm);
+  __shared__ unsigned long long twbar;
   lf_pdl_trigger();
-  stage_tree_async<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR,
-                       threadIdx.x, blockDim.x);
+  tw_bulk_begin<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
   lf_pdl_wait();
   // instances blockIdx.z*bpc .. +bpc-1 share the staged twiddles
   const size_t roff = ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2);
@@ -85,8 +85,7 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
     }
     if (b + 1 < b1) prefetch_l1(x + off + x_bs + (size_t)tl * C::E);
     if (b == b0) {
-      cp_async_wait_all();
-      __syncthreads();
+      tw_bulk_wait(&twbar);
     } else {
       __syncwarp();
     }
@@ -445,14 +444,13 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
     prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
   };
+  __shared__ unsigned long long twbar;
   lf_pdl_trigger();
   if (!A.pre)           // finished pieces need no row NTT here
-    stage_tree_async<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR,
-                         threadIdx.x, blockDim.x);
+    tw_bulk_begin<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR, &twbar);
   lf_pdl_wait();
   prefetch_digit(0);
-  cp_async_wait_all();
-  __syncthreads();
+  if (!A.pre) tw_bulk_wait(&twbar);
 
   u64 accb[C::E], acca[C::E];
 #pragma unroll
@@ -778,8 +776,9 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   const u32 sc = A.scal[t * A.sstride], scp = A.scal[t * A.sstride + 1];
   uint2* tws = reinterpret_cast<uint2*>(sm);
   const u32 R0 = (1u << L1) + (blockIdx.x % groups) * S::LPCR;
+  __shared__ unsigned long long twbar;
   lf_pdl_trigger();
-  stage_tree_async<L2>(tws, dv.twf + ((size_t)t << logN), R0, S::LPCR, threadIdx.x, blockDim.x);
+  tw_bulk_begin<L2>(tws, dv.twf + ((size_t)t << logN), R0, S::LPCR, &twbar);
   lf_pdl_wait();
   const TwTree tw{tws, R0, S::LPCR};
   u32* xs = rowpass_xs<L1, L2>(sm);
@@ -801,8 +800,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
     if (p || bb != b0) {
       __syncwarp();
     } else {
-      cp_async_wait_all();
-      __syncthreads();
+      tw_bulk_wait(&twbar);
     }
     fwd_line<L2, BIN>(cv, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
     load_row_step2<L2>(av, A.acc + b * A.acc_bs + ((size_t)(p * A.nacc + t) << logN) + lo0, tl);

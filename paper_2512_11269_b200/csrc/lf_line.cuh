@@ -100,6 +100,56 @@ LF_DEV void stage_tree_async(uint2* dst, const uint2* __restrict__ tab, u32 R0, 
   }
 }
 
+// TMA bulk-copy variant (cp.async.bulk, completion on an mbarrier): ONE thread issues one
+// bulk copy per tree depth; the other threads keep issuing their data loads.  Call
+// tw_bulk_begin from all threads (it contains the barrier that publishes the mbarrier init)
+// and tw_bulk_wait from all threads before the first twiddle read.  Depths whose extent is not
+// 16-byte aligned (tiny rings only) are copied by the issuing thread directly.
+LF_DEV void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(a), "r"(phase) : "memory");
+  }
+}
+
+template <int LP>
+LF_DEV void tw_bulk_begin(uint2* dst, const uint2* __restrict__ tab, u32 R0, int span,
+                          unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned tx = 0;
+#pragma unroll
+    for (int d = 0; d < LP; ++d) {
+      const uint2* src = tab + ((size_t)R0 << d);
+      uint2* o = dst + span * ((1 << d) - 1);
+      const unsigned bytes = (unsigned)(span << d) * 8u;
+      if ((bytes & 15u) == 0 && ((size_t)src & 15u) == 0 && ((size_t)o & 15u) == 0) tx += bytes;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+#pragma unroll
+    for (int d = 0; d < LP; ++d) {
+      const uint2* src = tab + ((size_t)R0 << d);
+      uint2* o = dst + span * ((1 << d) - 1);
+      const unsigned bytes = (unsigned)(span << d) * 8u;
+      if ((bytes & 15u) == 0 && ((size_t)src & 15u) == 0 && ((size_t)o & 15u) == 0) {
+        const unsigned so = (unsigned)__cvta_generic_to_shared(o);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(so), "l"(src), "r"(bytes), "r"(a) : "memory");
+      } else {
+        for (int i = 0; i < (span << d); ++i) o[i] = __ldg(&src[i]);
+      }
+    }
+  }
+  __syncthreads();
+}
+LF_DEV void tw_bulk_wait(unsigned long long* bar) { mbar_wait(bar, 0); }
+
 template <int M>
 LF_DEV void stage_flat(uint2* dst, const uint2* __restrict__ tab, int tid, int nthr) {
   for (int i = tid; i < M; i += nthr) dst[i] = __ldg(&tab[i]);
