@@ -88,6 +88,29 @@ int lf_ctx_create(int logN, int nprimes, const uint32_t* primes, const uint32_t*
       twi[(size_t)i * N + j] = make_uint2(iw, shoup(iw, q));
     }
   }
+  // Row-pass twiddle subtrees, transposed per CTA line block for the depths the second phase of
+  // a line transform reads (thread-varying roots): see TwTree<LP> in lf_line.cuh.
+  std::vector<uint2> twfT(twf), twiT(twi);
+  {
+    int L1, L2;
+    lf_split(logN, L1, L2);
+    const int DS = (L2 + 1) / 2;
+    int lpc = 256 / (1 << (L2 / 2));
+    if (lpc < 1) lpc = 1;
+    const int span = lpc < (1 << L1) ? lpc : (1 << L1);
+    for (int i = 0; i < nprimes; ++i)
+      for (int d = DS; d < L2; ++d) {
+        const int kk = d - DS, cnt = span << d;
+        for (int b = 0; b < (1 << L1) / span; ++b) {
+          const size_t c0 = (size_t)i * N + ((size_t)((1u << L1) + (u32)(b * span)) << d);
+          for (int off = 0; off < cnt; ++off) {
+            const size_t dst = c0 + (size_t)(off & ((1 << kk) - 1)) * (span << DS) + (off >> kk);
+            twfT[dst] = twf[c0 + off];
+            twiT[dst] = twi[c0 + off];
+          }
+        }
+      }
+  }
   LfCtx* c = new LfCtx();
   c->logN = logN;
   c->N = (int)N;
@@ -100,6 +123,10 @@ int lf_ctx_create(int logN, int nprimes, const uint32_t* primes, const uint32_t*
   LF_CUDA(cudaMemcpy(c->d_pk, pk.data(), sizeof(PrimeK) * nprimes, cudaMemcpyHostToDevice));
   LF_CUDA(cudaMemcpy(c->d_twf, twf.data(), sizeof(uint2) * twf.size(), cudaMemcpyHostToDevice));
   LF_CUDA(cudaMemcpy(c->d_twi, twi.data(), sizeof(uint2) * twi.size(), cudaMemcpyHostToDevice));
+  LF_CUDA(cudaMalloc(&c->d_twfT, sizeof(uint2) * twfT.size()));
+  LF_CUDA(cudaMalloc(&c->d_twiT, sizeof(uint2) * twiT.size()));
+  LF_CUDA(cudaMemcpy(c->d_twfT, twfT.data(), sizeof(uint2) * twfT.size(), cudaMemcpyHostToDevice));
+  LF_CUDA(cudaMemcpy(c->d_twiT, twiT.data(), sizeof(uint2) * twiT.size(), cudaMemcpyHostToDevice));
   *out = c;
   return 0;
 }
@@ -110,6 +137,8 @@ int lf_ctx_destroy(lf_ctx* ctx) {
   cudaFree(ctx->d_pk);
   cudaFree(ctx->d_twf);
   cudaFree(ctx->d_twi);
+  cudaFree(ctx->d_twfT);
+  cudaFree(ctx->d_twiT);
   delete[] ctx->h_pk;
   delete ctx;
   return 0;

@@ -12,6 +12,8 @@ struct LfDev {
   const PrimeK* pk;      // [nprimes]  per-prime constants
   const uint2* twf;      // [nprimes << logN]  {psi^brv(i), Shoup companion}
   const uint2* twi;      // [nprimes << logN]  {psi^-brv(i), Shoup companion}
+  const uint2* twfT;     // twf / twi with the row-pass subtrees of depth >= LineCfg<L2>::LA
+  const uint2* twiT;     //   stored transposed per CTA line block (TwTree<LP>, tw_bulk_begin)
   int logN;
   int nprimes;
 };
@@ -30,8 +32,10 @@ struct LfCtx {
   PrimeK* d_pk;
   uint2* d_twf;
   uint2* d_twi;
+  uint2* d_twfT;
+  uint2* d_twiT;
   PrimeK* h_pk;
-  LfDev dev() const { return LfDev{d_pk, d_twf, d_twi, logN, nprimes}; }
+  LfDev dev() const { return LfDev{d_pk, d_twf, d_twi, d_twfT, d_twiT, logN, nprimes}; }
 };
 
 // error plumbing (lf_api.cu)

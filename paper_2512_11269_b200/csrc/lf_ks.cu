@@ -67,7 +67,7 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   uint2* tws = reinterpret_cast<uint2*>(sm);
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
-  tw_bulk_begin<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
+  tw_bulk_begin<L2>(tws, dv.twiT + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
   lf_pdl_wait();
   // instances blockIdx.z*bpc .. +bpc-1 share the staged twiddles
   const size_t roff = ((size_t)((row / rpp) * src_rs + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2);
@@ -89,7 +89,7 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
     } else {
       __syncwarp();
     }
-    inv_line<L2>(v, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
+    inv_line<L2>(v, (1u << L1) + hi, TwTree<L2>{tws, (1u << L1) + hi0, S::LPCR}, pk.q,
                  rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
     store_row_step2<L2>(v, T0 + (size_t)b * t_bs + ((size_t)row << (L1 + L2)) + ((size_t)hi << L2), tl);
   }
@@ -447,7 +447,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
   if (!A.pre)           // finished pieces need no row NTT here
-    tw_bulk_begin<L2>(tws, dv.twf + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR, &twbar);
+    tw_bulk_begin<L2>(tws, dv.twfT + ((size_t)pi << logN), (1u << L1) + hi0s, S::LPCR, &twbar);
   lf_pdl_wait();
   prefetch_digit(0);
   if (!A.pre) tw_bulk_wait(&twbar);
@@ -489,7 +489,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     } else {
       const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
       load_row_step2<L2>(pc, tr, tl);
-      fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
+      fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree<L2>{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
                         tl, addr, SyncWarp{});
       if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
@@ -778,9 +778,9 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   const u32 R0 = (1u << L1) + (blockIdx.x % groups) * S::LPCR;
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
-  tw_bulk_begin<L2>(tws, dv.twf + ((size_t)t << logN), R0, S::LPCR, &twbar);
+  tw_bulk_begin<L2>(tws, dv.twfT + ((size_t)t << logN), R0, S::LPCR, &twbar);
   lf_pdl_wait();
-  const TwTree tw{tws, R0, S::LPCR};
+  const TwTree<L2> tw{tws, R0, S::LPCR};
   u32* xs = rowpass_xs<L1, L2>(sm);
   const AddrR<L2> addr{ln * pitchR<L2>()};
   const size_t lo0 = ((size_t)hi << L2);

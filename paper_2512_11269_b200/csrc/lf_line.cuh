@@ -63,11 +63,23 @@ struct TwGlobal {
   const uint2* p;
   LF_DEV uint2 get(int, u32 n) const { return __ldg(&p[n]); }
 };
+// Depths d >= LineCfg<LP>::LA are read in the second phase of a line transform, where the
+// threads of a line hold consecutive roots r (at depth LA) and read node (r << k) + blk: the
+// staged copy (from LfDev::twfT / twiT) holds them transposed, [blk][r], so a warp's reads hit
+// consecutive words instead of 2^k-strided ones (bank conflicts).
+template <int LP>
 struct TwTree {
   const uint2* s;
   u32 R0;
   int span;
-  LF_DEV uint2 get(int d, u32 n) const { return s[span * ((1 << d) - 1) + (n - (R0 << d))]; }
+  LF_DEV uint2 get(int d, u32 n) const {
+    constexpr int DS = LineCfg<LP>::LA;
+    const u32 off = n - (R0 << d);
+    const int base = span * ((1 << d) - 1);
+    if (d < DS) return s[base + off];
+    const int kk = d - DS;
+    return s[base + (int)(off & ((1u << kk) - 1)) * (span << DS) + (int)(off >> kk)];
+  }
 };
 struct TwFlat {
   const uint2* s;

@@ -41,12 +41,12 @@ k_ntt_fwd_R(u32* rows, RowMap rm, LfDev dv) {
   const int pi = rm.p[row];
   const PrimeK pk = dv.pk[pi];
   __shared__ unsigned long long twbar;
-  tw_bulk_begin<L2>(tws, dv.twf + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
+  tw_bulk_begin<L2>(tws, dv.twfT + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
   u32* base = rows + ((size_t)row << (L1 + L2)) + ((size_t)hi << L2);
   u32 x[C::E];
   load_row_step1<L2>(x, base, tl);
   tw_bulk_wait(&twbar);
-  fwd_line<L2, S::FWD_C_OUT>(x, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, pk.q, xs,
+  fwd_line<L2, S::FWD_C_OUT>(x, (1u << L1) + hi, TwTree<L2>{tws, (1u << L1) + hi0, S::LPCR}, pk.q, xs,
                              tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
 #pragma unroll
   for (int e = 0; e < C::E; ++e) x[e] = reduce32(x[e], pk);
@@ -67,12 +67,12 @@ k_ntt_inv_R(u32* rows, RowMap rm, LfDev dv) {
   const int pi = rm.p[row];
   const u32 q = dv.pk[pi].q;
   __shared__ unsigned long long twbar;
-  tw_bulk_begin<L2>(tws, dv.twi + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
+  tw_bulk_begin<L2>(tws, dv.twiT + ((size_t)pi << (L1 + L2)), (1u << L1) + hi0, S::LPCR, &twbar);
   u32* base = rows + ((size_t)row << (L1 + L2)) + ((size_t)hi << L2);
   u32 x[C::E];
   load_row_step2<L2>(x, base, tl);
   tw_bulk_wait(&twbar);
-  inv_line<L2>(x, (1u << L1) + hi, TwTree{tws, (1u << L1) + hi0, S::LPCR}, q, xs, tl,
+  inv_line<L2>(x, (1u << L1) + hi, TwTree<L2>{tws, (1u << L1) + hi0, S::LPCR}, q, xs, tl,
                AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
   store_row_step1<L2>(x, base, tl);
 }
