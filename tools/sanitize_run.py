@@ -1,6 +1,7 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck): desk-size
 keyswitch, hom_mul, rotate (hoisted, batched, extended), rescale (single, double), ModRaise,
-plaintext MACs and a toy bootstrap on cuda:0."""
+plaintext MACs, a toy bootstrap, the fused mul+rescale and BSGS kernels, the kernel-plan
+interpreter and the NTT row kernels (TMA-staged twiddles) on cuda:0."""
 import os
 import sys
 
@@ -32,5 +33,22 @@ ck, trk = BT.make_bootstrap_keys(tp, tsk, planner.required_rotations())
 tct = B.encrypt(B.encode(np.random.default_rng(3).uniform(-1, 1, tp.n), tp, level=0, scale=2 ** 22), tpk, tp,
                 np.random.default_rng(4))
 out = BT.Bootstrapper(BT.GpuBackend(tp, trlk, ck, trk), cfg).bootstrap(tct)
+# fused hom_mul + double rescale, fused BSGS inner sums, kernel-plan interpreter, NTT row kernels
+mr = fused.hom_mul_rescale(p, ct, ct, rlk, 2)
+fz = be.bsgs_fused_ext(ct, [(0, [(0, pt), (1, pt)]), (3, [(2, pt)])])
+import json  # noqa: E402
+from paper_2512_11269_b200.kernel_runner import KernelRunner, plan_from_json  # noqa: E402
+fx = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                 "tests", "golden", "kernel_plans_synth.json")))
+kp = B.gen_params(**fx["gen_params"])
+rows = {l: torch.randint(0, 1 << 20, (kp.N,), dtype=torch.int32, device="cuda") for l, _ in fx["inputs"]}
+kr = KernelRunner(kp)
+for pl in fx["plans"]:
+    kr.run(plan_from_json(pl), lambda l: rows[l],
+           lambda l: rows.setdefault(l, torch.empty(kp.N, dtype=torch.int32, device="cuda")))
+from paper_2512_11269_b200.poly import ntt_rows  # noqa: E402
+nr = torch.randint(0, 1 << 20, (4, p.N), dtype=torch.int32, device="cuda")
+ntt_rows(p, nr, (0, 1, 2, 3))
+ntt_rows(p, nr, (0, 1, 2, 3), inverse=True)
 torch.cuda.synchronize()
-print("sanitize run ok", m.level, len(r), out.level)
+print("sanitize run ok", m.level, len(r), out.level, mr[0].limbs.shape[0], fz.level)
