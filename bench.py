@@ -402,6 +402,47 @@ def rotation_units(params, level, dev, steps=5):
             "keys": "synthetic uniform rows (8 rotation keys, steps 1..8)"}
 
 
+def secondary_keyswitch(dev, B=32, steps=5):
+    """SURVEY §8d secondary C2: gen_params(65536, 24, d=3) (25 + 9 primes, ext 34), full-level
+    keyswitch at batch B; synthetic inputs and key rows (cost is data-independent)."""
+    import torch
+    from types import SimpleNamespace
+    import paper_2512_11269_b200 as Bk
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.context import get_context
+    p = Bk.gen_params(65536, 24, d=3, seed=0, scale=2 ** 26)
+    level, N = p.max_level, p.N
+    l1, alpha, d = level + 1, p.num_special, p.ks.d
+    primes = list(p.rns_basis) + list(p.special_basis)
+    g = torch.Generator(device=dev).manual_seed(99)
+
+    def rows(idx, lead=()):
+        q = torch.tensor([primes[i] for i in idx], dtype=torch.int64, device=dev)[:, None]
+        r = torch.randint(0, 2 ** 62, (*lead, len(idx), N), device=dev, generator=g, dtype=torch.int64)
+        return (r % q).to(torch.int32)
+    key = SimpleNamespace(data=rows(list(range(l1 + alpha)), (d, 2)).contiguous())
+    x = rows(list(range(l1)), (B,))
+    out = torch.empty((B, 2, l1, N), dtype=torch.int32, device=dev)
+    ws = get_context(p).ks_workspace(level, B)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    for _ in range(2):
+        fused.keyswitch_batch(p, level, x, key, out=out, ws=ws)
+    ms = 0.0
+    for i in range(steps):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fused.keyswitch_batch(p, level, x, key, out=out, ws=ws)
+        b.record()
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    us = ms / steps / B * 1e3
+    rows_alg = l1 + 2 * min(d, l1) * (l1 + alpha) + 2 * l1
+    return {"config": "gen_params(65536, 24, d=3): 25 main + 9 special, ext 34", "batch": B,
+            "keyswitch_us": us, "ops_per_s": 1e6 / us, "algorithmic_bytes": rows_alg * N * 4,
+            "hbm_gbs": rows_alg * N * 4 / (us * 1e-6) / 1e9}
+
+
 def ntt_summary(ntt, clocks):
     mhz = (clocks or {}).get("sm_mhz") or 1965
     peak = 32 * 148 * mhz * 1e6                  # IMAD.HI per second (one per butterfly)
@@ -566,6 +607,7 @@ def run_ours(args, rank, world):
     ntt = ntt_throughput(params, dev)
     sweep = batch_sweep(params, level, rlk, dev) if rank == 0 else None
     rot = rotation_units(params, level, dev) if rank == 0 else None
+    sec = secondary_keyswitch(dev) if rank == 0 else None
 
     sharded = None
     if world > 1:
@@ -606,6 +648,7 @@ def run_ours(args, rank, world):
             "ntt": ntt_summary(ntt, clocks),
             "batch_sweep": sweep,
             "rotation": rot,
+            "secondary_c2": sec,
             "limb_sharded": sharded,
         }
         print(json.dumps(line), flush=True)
