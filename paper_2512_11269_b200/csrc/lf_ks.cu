@@ -836,12 +836,21 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
       }
     } else if (EPI == EPI_ROT) {
       if (p == 0) {
-        const u32* br = A.e0 + b * A.e_bs + ((size_t)t << logN);
+        // + sigma_g(b): load the source line coalesced, permute it through the line's exchange
+        // buffer (bit-reversed slots: conflict-free), instead of a per-element global gather
+        const u32 g = A.gs[b];
+        const int hs = (int)(auto_src_index((u32)hi << L2, g, logN) >> L2);
+        u32 bv[C::E];
+        load_row_step2<L2>(bv, A.e0 + b * A.e_bs + ((size_t)t << logN) + ((size_t)hs << L2), tl);
+        u32* pb = xs + ln * pitchR<L2>();
+        __syncwarp();                       // the line transform's reads of xs are done
 #pragma unroll
-        for (int e = 0; e < C::E; ++e) {
-          const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-          av[e] = addmod(av[e], br[auto_src_index(pos, A.gs[b], logN)], pk.q);
-        }
+        for (int e = 0; e < C::E; ++e) pb[brev_bits(tl * C::E + e, L2)] = bv[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < C::E; ++e)
+          av[e] = addmod(av[e], pb[auto_src_slot_brev(((u32)hi << L2) + tl * C::E + e, g, logN, L2)], pk.q);
+        __syncwarp();                       // before the next line transform reuses xs
       }
     }
     store_row_step2<L2>(av, A.out + b * A.out_bs + ((size_t)(p * A.nt + t) << logN) + lo0, tl);
