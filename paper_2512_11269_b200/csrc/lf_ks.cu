@@ -477,14 +477,33 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
       const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
       const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
-      const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)t << logN);
+      if (GALOIS) {
+        // the source line, coalesced; sigma_g through the line's slot buffer (GMODE 1)
+        load_row_step2<L2>(pc, xr + ((size_t)hs << L2), tl);
 #pragma unroll
-      for (int e = 0; e < C::E; ++e) {
-        const u32 pos = ((u32)hi << L2) + tl * C::E + e;
-        const u32 src = KP ? ((u32)hs << L2) + tl * C::E + e : GALOIS ? auto_src_index(pos, gal, logN) : pos;
-        u32 v = xr[src];
-        if (XMODE == 1) v = mulmod(v, xr2[src], pk);
-        pc[e] = mul_shoup_lazy(v, s, sp, pk.q);
+        for (int e = 0; e < C::E; ++e) pc[e] = mul_shoup_lazy(pc[e], s, sp, pk.q);
+        if (!KP) {
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e < C::E; ++e) perm_buf[brev_bits(tl * C::E + e, L2)] = pc[e];
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e < C::E; ++e) {
+            const u32 pos = ((u32)hi << L2) + tl * C::E + e;
+            pc[e] = perm_buf[auto_src_slot_brev(pos, gal, logN, L2)];
+          }
+        }
+      } else {
+        const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)t << logN);
+        load_row_step2<L2>(pc, xr + ((size_t)hi << L2), tl);
+        if (XMODE == 1) {
+          u32 w[C::E];
+          load_row_step2<L2>(w, xr2 + ((size_t)hi << L2), tl);
+#pragma unroll
+          for (int e = 0; e < C::E; ++e) pc[e] = mulmod(pc[e], w[e], pk);
+        }
+#pragma unroll
+        for (int e = 0; e < C::E; ++e) pc[e] = mul_shoup_lazy(pc[e], s, sp, pk.q);
       }
     } else {
       const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
