@@ -995,13 +995,18 @@ static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax
   return launch_bc<L1, L2, CW8, 16, TG, 0>(ctx, A, batch, kmax, s);
 }
 
-static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax) {
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+static int bc_tsplit(int ngroups, int batch, int ncoltiles, int mmax, int limit = 96) {
   // Split the target range over a cluster only while the launch has fewer CTAs than ~2/3 of
   // the 148 SMs: each CTA then converts all its targets from one source tile (no DSMEM
   // exchange), which measured fastest whenever the grid already covers the GPU (C2 batch 1:
   // ModUp 75 -> 63 us unsplit; ModDown with 2 groups needs the split: 64 -> 43 us).
   int ts = 1;
-  while (ts < 8 && (long)ngroups * batch * ncoltiles * ts < 96 && mmax / (ts * 2) >= 4) ts *= 2;
+  while (ts < 8 && (long)ngroups * batch * ncoltiles * ts < limit && mmax / (ts * 2) >= 4) ts *= 2;
   return ts;
 }
 
@@ -1073,7 +1078,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
       kmax = K.up[j].B.k > kmax ? K.up[j].B.k : kmax;
       mmax = K.up[j].B.m > mmax ? K.up[j].B.m : mmax;
     }
-    A.tsplit = bc_tsplit(K.beta, nsh, (1 << L2) / 8, mmax);
+    A.tsplit = bc_tsplit(K.beta, nsh, (1 << L2) / 8, mmax, env_int("LF_TSPLIT_UP", 96));
     if (int e = launch_bc_auto<L1, L2>(ctx, A, nsh, kmax, s)) return e;
   }
   // hoisted batch: finish the NTT of every piece ONCE (in place, natural layout); each rotation's
@@ -1143,7 +1148,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
       A.g[p].src_row0 = p * alpha;
       A.g[p].dst_row0 = p * l1;
     }
-    A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, nt);
+    A.tsplit = bc_tsplit(2, c.batch, (1 << L2) / 8, nt, env_int("LF_TSPLIT_DOWN", 96));
     if (int e = launch_bc_auto<L1, L2>(ctx, A, c.batch, alpha + nd, s)) return e;
   }
   LF_MARK(4);
