@@ -607,7 +607,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
         ra[e] = addmod(ra[e], mul_shoup(d1, pm, pmp, pk.q), pk.q);
       }
     }
-    const uint2* tw = dv.twi + ((size_t)pi << logN);
+    const TwGlobalT<L2> tw{dv.twiT + ((size_t)pi << logN), (1u << L1) + (u32)((bl % groups) * S::LPCR), S::LPCR};
     __syncwarp();
     inv_line<L2>(rb, (1u << L1) + hi, tw, pk.q, xs, tl, addr, SyncWarp{});
     store_row_step2<L2>(rb, A.T2 + b * A.t2_bs + ((size_t)s << logN) + ((size_t)hi << L2), tl);

@@ -81,6 +81,22 @@ struct TwTree {
     return s[base + (int)(off & ((1u << kk) - 1)) * (span << DS) + (int)(off >> kk)];
   }
 };
+// TwTree's transposed layout read straight from the global copy (LfDev::twfT / twiT): the
+// CTA's line block starts at root R0 (a multiple of span); consecutive threads of the second
+// phase read consecutive entries (fewer L1 sectors than the natural table).
+template <int LP>
+struct TwGlobalT {
+  const uint2* p;
+  u32 R0;
+  int span;
+  LF_DEV uint2 get(int d, u32 n) const {
+    constexpr int DS = LineCfg<LP>::LA;
+    if (d < DS) return __ldg(&p[n]);
+    const u32 off = n - (R0 << d);
+    const int kk = d - DS;
+    return __ldg(&p[((size_t)R0 << d) + (off & ((1u << kk) - 1)) * (u32)(span << DS) + (off >> kk)]);
+  }
+};
 struct TwFlat {
   const uint2* s;
   LF_DEV uint2 get(int, u32 n) const { return s[n]; }
