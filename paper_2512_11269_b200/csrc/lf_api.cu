@@ -98,6 +98,19 @@ int lf_ctx_create(int logN, int nprimes, const uint32_t* primes, const uint32_t*
     int lpc = 256 / (1 << (L2 / 2));
     if (lpc < 1) lpc = 1;
     const int span = lpc < (1 << L1) ? lpc : (1 << L1);
+    // column tree (root 1, the first L1 levels; read through TwGlobalT<L1>{.., 1, 1} by the
+    // BConv column passes): its second-phase depths transposed the same way, span 1
+    const int DSc = (L1 + 1) / 2;
+    for (int i = 0; i < nprimes; ++i)
+      for (int d = DSc; d < L1; ++d) {
+        const int kk = d - DSc;
+        const size_t c0 = (size_t)i * N + ((size_t)1 << d);
+        for (int off = 0; off < (1 << d); ++off) {
+          const size_t dst = c0 + (size_t)(off & ((1 << kk) - 1)) * (1u << DSc) + (off >> kk);
+          twfT[dst] = twf[c0 + off];
+          twiT[dst] = twi[c0 + off];
+        }
+      }
     for (int i = 0; i < nprimes; ++i)
       for (int d = DS; d < L2; ++d) {
         const int kk = d - DS, cnt = span << d;

@@ -269,7 +269,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
     load_col_step2<L1, L2>(x, src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col, tl);
-    inv_line<L1>(x, 1u, dv.twi + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
+    inv_line<L1>(x, 1u, TwGlobalT<L1>{dv.twiT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
     for (int j = 0; j < E; ++j) x[j] = mul_shoup(x[j], ci, cpi, pk.q);
@@ -354,7 +354,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 #pragma unroll
       for (int j = 0; j < EH; ++j) x[h * EH + j] = reduce64_lazy4(acc[j], pk);
     }
-    fwd_line<L1, 4>(x, 1u, dv.twf + ((size_t)pi << logN), pk.q, X, tl, addr, gsync);
+    fwd_line<L1, 4>(x, 1u, TwGlobalT<L1>{dv.twfT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
     store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
     gsync();
   }
