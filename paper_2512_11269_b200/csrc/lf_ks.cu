@@ -906,7 +906,9 @@ k_pieces(const u32* T1, const u32* __restrict__ x, u32* out,
     for (int e = 0; e < C::E; ++e) v[e] = mul_shoup(v[e], rowk[4 * t], rowk[4 * t + 1], pk.q);
   } else {
     load_row_step2<L2>(v, T1 + ((size_t)r << logN) + lo0, tl);
-    fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi, dv.twf + ((size_t)pi << logN), pk.q,
+    fwd_line<L2, S::FWD_C_OUT>(v, (1u << L1) + hi,
+                               TwGlobalT<L2>{dv.twfT + ((size_t)pi << logN),
+                                             (1u << L1) + (u32)((blockIdx.x % groups) * S::LPCR), S::LPCR}, pk.q,
                                rowpass_xs<L1, L2>(sm), tl, AddrR<L2>{ln * pitchR<L2>()}, SyncWarp{});
 #pragma unroll
     for (int e = 0; e < C::E; ++e) v[e] = reduce32(v[e], pk);
