@@ -272,7 +272,7 @@ class BootConfig:
     cheb_degree: int = 31
     baby: int = 8                # Chebyshev baby steps T_0..T_7
     lazy_moddown: bool = True    # BSGS: one ModDown per giant step instead of per rotation
-    bsgs_ratio: int = 4          # giant/baby cost ratio used to size the baby steps
+    bsgs_ratio: int = 8          # giant/baby cost ratio used to size the baby steps (swept: DESIGN §6)
 
 
 def evalmod_constants(cfg: BootConfig):
