@@ -118,6 +118,14 @@ class OracleBackend:
             acc = c if acc is None else O.hom_add(P, acc, c)
         return acc
 
+    def with_scale(self, x, scale):
+        r = map_batch(lambda c: self.with_scale(c, scale), x)
+        if r is not None:
+            return r
+        import dataclasses
+        from fractions import Fraction
+        return dataclasses.replace(x, scale=Fraction(scale))
+
     def add(self, x, y):
         r = map_batch(self.add, x, y)
         if r is not None:

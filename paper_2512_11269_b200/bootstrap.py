@@ -433,14 +433,15 @@ class Bootstrapper:
         T = {1: u}
         g = self.cfg.baby
 
+        def twice(x):                           # 2x: the same residues at half the scale
+            return be.with_scale(x, Fraction(x.scale) / 2)
+
         def double(k):                          # T_2k = 2 T_k^2 - 1
-            x = self._mul2(T[k], T[k])
-            x = be.add(x, x)
+            x = twice(self._mul2(T[k], T[k]))
             return be.add_const(x, -1.0)
 
         def odd(k):                             # T_2k+1 = 2 T_k T_k+1 - T_1
-            x = self._mul2(T[k], T[k + 1])
-            x = be.add(x, x)
+            x = twice(self._mul2(T[k], T[k + 1]))
             return be.sub(x, self._match(T[1], x.level, x.scale))
 
         for m in range(2, g):
@@ -904,6 +905,12 @@ class GpuBackend:
         return self.C.Ciphertext(acc.b, acc.a, scale, level)
 
     # arithmetic
+    def with_scale(self, x, scale):
+        """The same residues declared at another scale (exact: value = residues / scale)."""
+        if isinstance(x, CtBatch):
+            return CtBatch(x.data, scale, x.level)
+        return self.C.Ciphertext(x.b, x.a, Fraction(scale), x.level)
+
     def _b_ewise(self, op, x, y):
         import torch
         from .poly import ewise
