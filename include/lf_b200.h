@@ -236,6 +236,10 @@ int lf_ptmac(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint3
  * mod the row's prime).  Equals poly_scalar_mul + poly_add (poly.py:183-209) term by term. */
 int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
                const uint32_t* const* a, const uint32_t* k, void* stream);
+/* lf_lincomb plus a per-row constant cb[r] (HOST array, any uint32) added to the b rows:
+ * sum_i k_i * ct_i + (cb, 0), i.e. then an add of a constant plaintext (ckks.py:152-179). */
+int lf_lincomb_c(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+                 const uint32_t* const* a, const uint32_t* k, const uint32_t* cb, void* stream);
 
 /* LFHE wire rows (little-endian uint64, reference serial.py:1-14, 63-69) <-> device uint32
  * residues, n words, both pointers on the device. */

@@ -158,10 +158,13 @@ class OracleBackend:
     def unstack(self, x):
         return list(x.cts)
 
-    def lincomb(self, terms):
+    def lincomb(self, terms, const=None):
+        """sum_i round(c_i S_i) ct_i, then (const) + round(const * scale) on b."""
         if isinstance(terms[0][0], ListBatch):
             B = len(terms[0][0].cts)
-            return ListBatch([self.lincomb([(t.cts[i], c, S) for t, c, S in terms]) for i in range(B)])
+            return ListBatch([self.lincomb([(t.cts[i], c, S) for t, c, S in terms], const) for i in range(B)])
+        if const is not None:
+            return self.add_const(self.lincomb(terms), const)
         acc = None
         for ct, c, S in terms:
             t = self.mul_const(ct, c, S)

@@ -73,6 +73,9 @@ def _load():
         "lf_lincomb": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                                       _u32_host, ctypes.c_void_p]),
+        "lf_lincomb_c": (ctypes.c_int, [ctypes.c_void_p, _u32p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                        _u32_host, _u32_host, ctypes.c_void_p]),
         "lf_rows_from_u64": (ctypes.c_int, [_u32p, _u32p, ctypes.c_size_t, ctypes.c_void_p]),
         "lf_rows_to_u64": (ctypes.c_int, [_u32p, _u32p, ctypes.c_size_t, ctypes.c_void_p]),
         "lf_rotate_hoisted_ext": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u32p, ctypes.c_int, _u32_host,

@@ -467,9 +467,10 @@ class Bootstrapper:
             S_p = Fraction(scale) * self.q[level + 2] * self.q[level + 1] / Fraction(t.scale)
             terms.append((t, float(c[i]), S_p))
         assert terms
-        acc = be.rescale2(be.lincomb(terms))
+        # the constant term joins the linear combination (before the double rescale)
+        acc = be.rescale2(be.lincomb(terms, const=float(c[0])))
         assert acc.level == level and acc.scale == scale
-        return be.add_const(acc, float(c[0]))
+        return acc
 
     def _feasible(self, c, T, t):
         g = self.cfg.baby
@@ -1010,15 +1011,16 @@ class GpuBackend:
     def conjugate(self, x):
         return self.C.hom_conjugate(x, self.ck, self.params)
 
-    def lincomb(self, terms, out=None):
-        """sum_i round(c_i S_i) * ct_i, all ct_i at one level with equal ct_i.scale * S_i."""
+    def lincomb(self, terms, out=None, const=None):
+        """sum_i round(c_i S_i) * ct_i, all ct_i at one level with equal ct_i.scale * S_i;
+        `const` adds round(const * scale) to b in the same pass (lf_lincomb_c)."""
         import torch
         if isinstance(terms[0][0], CtBatch):
             t0 = terms[0][0]
             B = t0.data.shape[0]
             out = torch.empty((B, 2, t0.level + 1, self.N), dtype=torch.int32, device=t0.data.device)
             for i in range(B):       # per instance, straight into the batch (views, no copies)
-                self.lincomb([(self.unstack(t)[i], c, S) for t, c, S in terms], out=out[i])
+                self.lincomb([(self.unstack(t)[i], c, S) for t, c, S in terms], out=out[i], const=const)
             return CtBatch(out, Fraction(t0.scale) * Fraction(terms[0][2]), t0.level)
         from . import _native
         from .context import get_context, stream_handle
@@ -1043,8 +1045,14 @@ class GpuBackend:
             bp = (ctypes_void_p * n)(*[ct.b.limbs.data_ptr() for ct, _, _ in chunk])
             ap = (ctypes_void_p * n)(*[ct.a.limbs.data_ptr() for ct, _, _ in chunk])
             from . import _native as nat
-            _native.check(nat.lib().lf_lincomb(ctx.handle, ctypes_void_p(tgt.data_ptr()), nrows, n, bp, ap,
-                                               nat.u32_array(ks), stream_handle()), "lf_lincomb")
+            if const is not None and i0 == 0:
+                kc = round(Fraction(const) * scale)
+                _native.check(nat.lib().lf_lincomb_c(ctx.handle, ctypes_void_p(tgt.data_ptr()), nrows, n, bp, ap,
+                                                     nat.u32_array(ks), nat.u32_array([kc % q for q in qs]),
+                                                     stream_handle()), "lf_lincomb_c")
+            else:
+                _native.check(nat.lib().lf_lincomb(ctx.handle, ctypes_void_p(tgt.data_ptr()), nrows, n, bp, ap,
+                                                   nat.u32_array(ks), stream_handle()), "lf_lincomb")
             if out is None:
                 out = tgt
             else:

@@ -261,7 +261,17 @@ int lf_lincomb(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uin
   if (nrows < 1 || nrows > ctx->nprimes || nrows > LF_LINCOMB_ROWS) { lf_set_error("lf_lincomb: bad nrows %d", nrows); return 2; }
   for (int i = 0; i < nterm; ++i)
     if (!b[i] || !a[i]) { lf_set_error("lf_lincomb: null term %d", i); return 1; }
-  return lf_launch_lincomb(ctx, out, nrows, nterm, b, a, k, (cudaStream_t)stream);
+  return lf_launch_lincomb(ctx, out, nrows, nterm, b, a, k, nullptr, (cudaStream_t)stream);
+}
+
+int lf_lincomb_c(const lf_ctx* ctx, uint32_t* out, int nrows, int nterm, const uint32_t* const* b,
+                 const uint32_t* const* a, const uint32_t* k, const uint32_t* cb, void* stream) {
+  if (!ctx || !out || !b || !a || !k || !cb) { lf_set_error("lf_lincomb_c: null argument"); return 1; }
+  if (nterm < 1 || nterm > LF_LINCOMB_MAX) { lf_set_error("lf_lincomb_c: nterm %d outside [1, %d]", nterm, LF_LINCOMB_MAX); return 2; }
+  if (nrows < 1 || nrows > ctx->nprimes || nrows > LF_LINCOMB_ROWS) { lf_set_error("lf_lincomb_c: bad nrows %d", nrows); return 2; }
+  for (int i = 0; i < nterm; ++i)
+    if (!b[i] || !a[i]) { lf_set_error("lf_lincomb_c: null term %d", i); return 1; }
+  return lf_launch_lincomb(ctx, out, nrows, nterm, b, a, k, cb, (cudaStream_t)stream);
 }
 
 int lf_rows_from_u64(uint32_t* out, const uint64_t* in, size_t n, void* stream) {

@@ -175,6 +175,7 @@ struct LinCombArgs {
   const u32* b[LF_LINCOMB_MAX];
   const u32* a[LF_LINCOMB_MAX];
   u32 k[LF_LINCOMB_MAX][LF_LINCOMB_ROWS];
+  u32 c0[LF_LINCOMB_ROWS];   // constant added to the b rows (0 when none)
 };
 
 __global__ void __launch_bounds__(256) k_lincomb(LinCombArgs A, LfDev dv) {
@@ -187,7 +188,8 @@ __global__ void __launch_bounds__(256) k_lincomb(LinCombArgs A, LfDev dv) {
   const size_t off = (size_t)r * N;
   for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < N / 4;
        v += (size_t)gridDim.x * blockDim.x) {
-    u64 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    const u64 c0 = p ? 0u : A.c0[r];
+    u64 acc0 = c0, acc1 = c0, acc2 = c0, acc3 = c0;
     for (int i = 0; i < A.nterm; ++i) {
       const u32* src = p ? A.a[i] : A.b[i];
       const uint4 x = reinterpret_cast<const uint4*>(src + off)[v];
@@ -203,9 +205,10 @@ __global__ void __launch_bounds__(256) k_lincomb(LinCombArgs A, LfDev dv) {
 }
 
 int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
-                      const u32* const* a, const u32* k, cudaStream_t s) {
+                      const u32* const* a, const u32* k, const u32* cb, cudaStream_t s) {
   LinCombArgs A;
   A.out = out; A.nterm = nterm; A.nrows = nrows;
+  for (int r = 0; r < nrows; ++r) A.c0[r] = cb ? cb[r] % ctx->h_pk[r].q : 0u;
   for (int i = 0; i < nterm; ++i) {
     A.b[i] = b[i]; A.a[i] = a[i];
     for (int r = 0; r < nrows; ++r) A.k[i][r] = k[(size_t)i * nrows + r] % ctx->h_pk[r].q;

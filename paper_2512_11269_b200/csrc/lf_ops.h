@@ -18,7 +18,7 @@ int lf_launch_ptmac(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32*
 #define LF_LINCOMB_MAX 8
 #define LF_LINCOMB_ROWS 64
 int lf_launch_lincomb(const LfCtx* ctx, u32* out, int nrows, int nterm, const u32* const* b,
-                      const u32* const* a, const u32* k, cudaStream_t s);
+                      const u32* const* a, const u32* k, const u32* cb, cudaStream_t s);
 int lf_launch_convert(void* out, const void* in, size_t n, bool narrow, cudaStream_t s);
 int lf_launch_mul_compressed(const LfCtx* ctx, u32* out, const u32* ct, const u32* uq, int nrows,
                              int ucount, int lb, cudaStream_t s);
