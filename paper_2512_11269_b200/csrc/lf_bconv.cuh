@@ -23,6 +23,11 @@ struct BconvDev {
   const u32* w;          // [m*k] (S/s_i) mod t, target-major: w[t*k + i]
   const u32* shat;       // [k*W] S/s_i as W little-endian 32-bit words
   const u32* S;          // [W]   S as W words
+  // tensor-core form (k_bconv_tc), or null: per target t, 4 rows b = 0..3 of K bytes with
+  // B[t][b][4i+a] = byte b of (2^(8a) (S/s_i) mod t) and B[t][b][4k] = byte b of negS[t], stored
+  // as the UMMA canonical K-major operand (pairs of targets = 8-row core-matrix groups, 512 B)
+  const unsigned char* w8;
+  int kb;                // A-operand bytes per row the table was built for (48 or 64)
 };
 
 // Word offsets inside the blob (u32 units; inv_s first so the doubles are 8-byte aligned).
@@ -41,6 +46,8 @@ __host__ __device__ inline BconvDev lf_bconv_view(const u32* base, int k, int m,
   b.w = base + 5 * k + 2 * m;
   b.shat = base + 5 * k + 2 * m + (size_t)k * m;
   b.S = b.shat + (size_t)k * W;
+  b.w8 = nullptr;
+  b.kb = 0;
   return b;
 }
 

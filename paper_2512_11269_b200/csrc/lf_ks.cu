@@ -24,6 +24,7 @@
 #include "lf_bconv.cuh"
 #include "lf_plan.h"
 #include "lf_ops.h"
+#include "lf_umma.cuh"
 
 #define LF_BC_MAXG 16
 #define LF_LAUNCH_CHECK(call)                                                  \
@@ -358,6 +359,187 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
     gsync();
   }
+  if (cl > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // peers done with my tile
+}
+
+// ---------------------------------------------------------------------------------------
+// K_BC on the 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+//
+// The base-conversion MAC of a target t over the k converted sources, Σ_i y_i·w_ti − u·S, is
+// computed mod t as a u8 x u8 -> s32 GEMM: with y_i = Σ_a y_ia 2^(8a) (bytes) and the weights
+// pre-multiplied and split on the host, w'_tiab = byte b of 2^(8a) w_ti mod t,
+//     S_tb = Σ_(i,a) y_ia w'_tiab  (+ u · byte b of negS_t),     X_t = Σ_b S_tb 2^(8b)
+// and X_t ≡ Σ_i y_i w_ti + u·negS_t (mod t), X_t < 2^46.  The A operand (one row per
+// coefficient, K = 4k+1 bytes: the k sources as little-endian u32 and u) IS the source tile:
+// phase 1 writes the converted sources straight into the UMMA canonical layout.  M-tile e
+// (128 rows) holds element e of every thread of a 128-thread group, so TMEM lane lt is the
+// coefficient thread lt of every group needs: each group reads 4 columns per element for its
+// own target.  One CTA per SM: 8 groups (1024 threads) x 8 targets per round, 16 M-tiles x
+// (8 targets x 4 bytes) = 512 TMEM columns; the MMAs of round r+1 run during the NTT column
+// passes of round r.  Replaces 10 IMAD.WIDE per target element (the fmaheavy-bound part of
+// k_bconv_colpass) with ~6 ALU ops and a quarter of a tcgen05.ld.
+template <int L1, int L2, int KB>
+__global__ void __launch_bounds__(1024, 1)
+k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
+  using C = LineCfg<L1>;
+  constexpr int E = C::E, T = C::T;
+  constexpr int CW = 8, TG = 8, GT = CW * T;
+  static_assert(GT == 128 && E == 16, "k_bconv_tc expects 16 x 16 column lines");
+  constexpr int NCT = (1 << L2) / CW;
+  constexpr int logN = L1 + L2;
+  constexpr int SBO = KB / 16 * 128;            // bytes per 8-row group of the A operand
+  constexpr int MT = 16 * SBO;                  // bytes per M-tile (128 rows)
+  constexpr int ABYTES = E * MT + 128;          // + tail met by the aliased 4th K-chunk (KB = 48)
+  extern __shared__ __align__(1024) unsigned char smb[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase_s;
+  unsigned char* As = smb;
+  unsigned char* Ws = smb + ABYTES;
+  const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
+  const int c = lt % CW, tl = lt / CW;
+  u32* X = reinterpret_cast<u32*>(Ws + wbytes) + grp * smemC_words<L1, CW>();
+  int bid = blockIdx.x;
+  const int ts = bid % A.tsplit;
+  bid /= A.tsplit;
+  const int b = bid % nbatch;
+  bid /= nbatch;
+  const int ct = bid % NCT;
+  const BcGroupDev& G = A.g[bid / NCT];
+  const BconvDev& B = G.B;
+  const int k = B.k;
+  const int col = ct * CW + c;
+  const u32* src = A.src + (size_t)b * A.src_bs;
+  u32* dst = A.dst + (size_t)b * A.dst_bs;
+  const AddrC<L1, CW> addr{c};
+  const SyncGroup<true> gsync{1 + grp, GT};
+  // this thread's row inside an M-tile: byte offset of 16-byte K-chunk 0
+  const int rowoff = (lt / 8) * SBO + (lt % 8) * 16;
+  auto yword = [&](int e, int i) -> u32* {
+    return reinterpret_cast<u32*>(As + e * MT + rowoff + (i / 4) * 128 + (i % 4) * 4);
+  };
+
+  // targets of this CTA: an even-aligned chunk (target pairs are 512-byte operand blocks)
+  const int chunk = ((B.m + A.tsplit - 1) / A.tsplit + 1) & ~1;
+  const int t0 = min(B.m, ts * chunk), t1 = min(B.m, t0 + chunk);
+  const int nrounds = (t1 - t0 + TG - 1) / TG;
+  lf_pdl_trigger();
+  {   // weights of [t0, t1) -> Ws (zero beyond), TMEM, mbarrier
+    const uint4* wsrc = reinterpret_cast<const uint4*>(B.w8 + (size_t)t0 * 256);
+    const int nw = (t1 - t0 + 1) / 2 * 32, nz = nrounds * TG / 2 * 32;
+    uint4* wd = reinterpret_cast<uint4*>(Ws);
+    for (int v = threadIdx.x; v < nz; v += blockDim.x) wd[v] = v < nw ? __ldg(wsrc + v) : make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 32) tmem_alloc(&tbase_s, 512);
+    if (threadIdx.x == 0) mbar_init(&mbar, 1);
+  }
+  lf_pdl_wait();
+
+  // phase 1: INTT column pass of each source, times c_i, into the A operand (rows = lanes)
+  const int cl = A.tsplit;
+  for (int i = ts + cl * grp; i < k; i += cl * TG) {
+    const int pi = B.src_pi[i];
+    const PrimeK pk = dv.pk[pi];
+    u32 x[E];
+    load_col_step2<L1, L2>(x, src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col, tl);
+    inv_line<L1>(x, 1u, TwGlobalT<L1>{dv.twiT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
+    const u32 ci = B.c[i], cpi = B.cp[i];
+#pragma unroll
+    for (int e = 0; e < E; ++e) *yword(e, i) = mul_shoup(x[e], ci, cpi, pk.q);
+    gsync();
+  }
+  if (cl > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    for (int i = 0; i < k; ++i) {
+      const int r = i % cl;
+      if (r == ts) continue;
+      for (int v = threadIdx.x; v < E * GT; v += blockDim.x) {
+        const int e = v / GT, l2 = v % GT;
+        u32* loc = reinterpret_cast<u32*>(As + e * MT + (l2 / 8) * SBO + (l2 % 8) * 16 + (i / 4) * 128 + (i % 4) * 4);
+        const unsigned la = (unsigned)__cvta_generic_to_shared(loc);
+        unsigned ra, q;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
+        asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(q) : "r"(ra) : "memory");
+        *loc = q;
+      }
+    }
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // done reading peers
+  }
+  __syncthreads();
+
+  // phase 2: exact overflow count u of each element (only group 0's 128 threads hold distinct
+  // rows; the 8 groups split the 16 M-tiles) -> K-row 4k of the A operand
+  for (int e = grp; e < E; e += TG) {
+    double v = 0.0;
+    for (int i = 0; i < k; ++i) v = fma((double)*yword(e, i), B.inv_s[i], v);
+    const double r = rint(v);
+    u32 uj;
+    if (fabs(v - r) >= 0x1p-40) {
+      uj = (u32)floor(v);
+    } else {
+      u32 yy[64];
+      bool z = true;
+      for (int i = 0; i < k; ++i) { yy[i] = *yword(e, i); z &= yy[i] == 0; }
+      uj = z ? 0u : bconv_u_exact(yy, B, (u32)r);
+    }
+    *yword(e, k) = uj;
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase_s;
+  const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(As), w0 = (uint32_t)__cvta_generic_to_shared(Ws);
+  constexpr uint32_t IDESC = umma_idesc_u8(128, 32);
+  auto issue = [&](int r) {
+#pragma unroll 1
+    for (int e = 0; e < E; ++e)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+        umma_i8(tmem + 32 * e, umma_sdesc(a0 + e * MT + 256 * s2, 128, SBO),
+                umma_sdesc(w0 + r * 2048 + 256 * s2, 128, 512), IDESC, s2 > 0);
+    umma_commit(&mbar);
+  };
+  if (threadIdx.x == 0 && nrounds > 0) issue(0);
+
+  // phase 3: per round, group g takes target t0 + 8 r + g: S_b from TMEM -> X mod t (lazy) ->
+  // NTT column pass -> destination row
+  const uint32_t tlane = tmem + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) + 4 * grp;
+#pragma unroll 1
+  for (int r = 0; r < nrounds; ++r) {
+    mbar_wait(&mbar, r & 1);
+    tc_fence_after();
+    const int t = t0 + TG * r + grp;
+    const bool active = t < t1;                          // uniform over the group's 4 warps
+    u32 x[E];
+    PrimeK pk;
+    if (active) {
+      pk = dv.pk[B.tgt_pi[t]];
+#pragma unroll
+      for (int h = 0; h < E / 4; ++h) {
+        u32 s[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tmem_ld4(tlane + 32 * (4 * h + j), s[j][0], s[j][1], s[j][2], s[j][3]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const u32 lo = s[j][0] + (s[j][1] << 8), z = s[j][2] + (s[j][3] << 8);
+          x[4 * h + j] = reduce64_lazy4((u64)lo + ((u64)z << 16), pk);
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();                                     // TMEM free for the next round
+    if (threadIdx.x == 0 && r + 1 < nrounds) {
+      tc_fence_after();
+      issue(r + 1);
+    }
+    if (active) {
+      fwd_line<L1, 4>(x, 1u, TwGlobalT<L1>{dv.twfT + ((size_t)B.tgt_pi[t] << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
+      store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
   if (cl > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // peers done with my tile
 }
 
@@ -974,12 +1156,44 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
   return 0;
 }
 
+static int env_int(const char* name, int dflt);
+
+template <int L1, int L2, int KB>
+static int launch_bc_tc(const LfCtx* ctx, const BcArgs& A, int batch, cudaStream_t s) {
+  constexpr int SBO = KB / 16 * 128;
+  constexpr size_t ABYTES = (size_t)16 * 16 * SBO + 128;
+  int mmax = 0;
+  for (int g = 0; g < A.ngroups; ++g) mmax = A.g[g].B.m > mmax ? A.g[g].B.m : mmax;
+  const int chunk = ((mmax + A.tsplit - 1) / A.tsplit + 1) & ~1;
+  const int wbytes = (chunk + 7) / 8 * 8 * 256;
+  const size_t sm = ABYTES + wbytes + (size_t)8 * smemC_words<L1, 8>() * 4;
+  if (sm > 227 * 1024) { lf_set_error("bconv_tc: shared memory %zu too large", sm); return 2; }
+  auto kern = k_bconv_tc<L1, L2, KB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const long nblocks = (long)batch * ((1 << L2) / 8) * A.ngroups * A.tsplit;
+  LfDev dv = ctx->dev();
+  LF_LAUNCH_CHECK(lf_launch(kern, dim3((unsigned)nblocks), dim3(1024), sm, s, A.tsplit, A, dv, batch, wbytes));
+  return 0;
+}
+
 // Column tile width and group count: CW = 8 columns (32-byte row segments) and four thread
 // groups sharing the source tile for the production sizes; narrower tiles for large digit
 // counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches with at most 12
-// sources per group use the compile-time-K kernel.
+// sources per group use the compile-time-K kernel.  With byte-split weight tables (k <= 15)
+// the conversion runs on the tensor cores (k_bconv_tc; LF_BC_TC=0 selects the IMAD kernel).
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
+  if constexpr (L1 == 8 && L2 == 8) {
+    static const int use_tc = env_int("LF_BC_TC", 1);
+    bool tc = use_tc != 0;
+    int kb = 0;
+    for (int g = 0; g < A.ngroups && tc; ++g) {
+      tc = A.g[g].B.w8 != nullptr;
+      kb = A.g[g].B.kb > kb ? A.g[g].B.kb : kb;
+    }
+    if (tc && kb == 48) return launch_bc_tc<L1, L2, 48>(ctx, A, batch, s);
+    if (tc && kb == 64) return launch_bc_tc<L1, L2, 64>(ctx, A, batch, s);
+  }
   constexpr int NCOL = 1 << L2;
   constexpr int CW8 = NCOL >= 8 ? 8 : NCOL;
   constexpr int TG = (CW8 * LineCfg<L1>::T) % 32 == 0 ? 4 : 1;

@@ -49,7 +49,37 @@ struct Blob {
 struct TabRec {
   size_t off;
   int k, m, W;
+  size_t w8off;            // word offset of the tensor-core byte table (0: none)
+  int kb;
 };
+
+// Byte-split weights of the tensor-core base conversion (BconvDev::w8): for target t and
+// output byte b, K-row [4i+a] = byte b of 2^(8a) (S/s_i) mod t, [4k] = byte b of negS[t].
+// Layout: target pair p = t/2 is one 512-byte block of four 16-byte K-chunks x 8 rows
+// (row (t%2)*4 + b), the canonical no-swizzle K-major UMMA operand (lf_umma.cuh).
+size_t build_w8(Blob& b, const std::vector<u32>& primes, const std::vector<int>& tgt, int k,
+                const std::vector<u32>& w, const std::vector<u32>& negS, int& kb) {
+  const int m = (int)tgt.size();
+  kb = 4 * k + 1 <= 48 ? 48 : 64;
+  const int mp = (m + 1) & ~1;
+  std::vector<unsigned char> bytes((size_t)mp * 256, 0);
+  for (int t = 0; t < m; ++t) {
+    const u32 q = primes[tgt[t]];
+    for (int K = 0; K <= 4 * k; ++K) {
+      u32 v;
+      if (K == 4 * k) v = negS[t];
+      else v = (u32)(((u64)w[(size_t)t * k + K / 4] << (8 * (K % 4))) % q);
+      for (int bb = 0; bb < 4; ++bb)
+        bytes[(size_t)(t / 2) * 512 + (K / 16) * 128 + ((t % 2) * 4 + bb) * 16 + K % 16] = (v >> (8 * bb)) & 255;
+    }
+  }
+  while (b.w.size() % 4) b.w.push_back(0);        // 16-byte aligned
+  const size_t off = b.w.size();
+  std::vector<u32> words(bytes.size() / 4);
+  memcpy(words.data(), bytes.data(), bytes.size());
+  b.push(words);
+  return off;
+}
 
 // Exact base-conversion table (layout lf_bconv_view).  `mult[i]` is folded into c_i.
 TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<int>& src,
@@ -59,7 +89,7 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
   for (int i : src) big_mul(S, primes[i]);
   while (S.size() > 1 && S.back() == 0) S.pop_back();
   const int W = (int)S.size() + 1;
-  TabRec r{b.align2(), k, m, W};
+  TabRec r{b.align2(), k, m, W, 0, 0};
   std::vector<u32> v;
   for (int i = 0; i < k; ++i) {
     double inv = 1.0 / (double)primes[src[i]];
@@ -69,7 +99,7 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
     v.push_back(two[1]);
   }
   for (int i = 0; i < k; ++i) v.push_back((u32)src[i]);
-  std::vector<u32> c(k);
+  std::vector<u32> c(k), negS(m), wts((size_t)m * k);
   for (int i = 0; i < k; ++i) {
     const u32 s = primes[src[i]];
     u32 hat = 1;                                   // (S/s_i) mod s_i
@@ -84,7 +114,8 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
     const u32 q = primes[tgt[t]];
     u32 sm = 1;
     for (int i = 0; i < k; ++i) sm = mulm(sm, primes[src[i]] % q, q);
-    v.push_back((q - sm) % q);
+    negS[t] = (q - sm) % q;
+    v.push_back(negS[t]);
   }
   for (int t = 0; t < m; ++t) {
     const u32 q = primes[tgt[t]];
@@ -92,6 +123,7 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
       u32 h = 1;
       for (int j = 0; j < k; ++j)
         if (j != i) h = mulm(h, primes[src[j]] % q, q);
+      wts[(size_t)t * k + i] = h;
       v.push_back(h);
     }
   }
@@ -106,6 +138,7 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
   Sw.resize(W, 0);
   v.insert(v.end(), Sw.begin(), Sw.end());
   b.push(v);
+  if (4 * k + 1 <= 64) r.w8off = build_w8(b, primes, tgt, k, wts, negS, r.kb);
   return r;
 }
 
@@ -251,7 +284,11 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
     return 3;
   }
   const u32* base = (const u32*)dmem;
-  auto view = [&](const TabRec& r) { return lf_bconv_view(base + r.off, r.k, r.m, r.W); };
+  auto view = [&](const TabRec& r) {
+    BconvDev v = lf_bconv_view(base + r.off, r.k, r.m, r.W);
+    if (r.w8off) { v.w8 = (const unsigned char*)(base + r.w8off); v.kb = r.kb; }
+    return v;
+  };
 
   LfKsPlan* P = new LfKsPlan();
   P->n_main = n_main;
