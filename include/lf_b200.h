@@ -47,6 +47,12 @@ typedef struct LfCtx lf_ctx;
 int lf_abi_version(void);
 const char* lf_last_error(void);
 
+/* Base-conversion engine of every fused pipeline (no reference counterpart: an execution
+ * choice, results are bit-identical): 1 = tcgen05 kind::i8 tensor cores with byte-split
+ * weights (default; env LF_BC_TC=0 starts with 0), 0 = IMAD.WIDE kernel.  Process-wide. */
+int lf_set_bconv_engine(int engine);
+int lf_get_bconv_engine(void);
+
 /* Context: per-prime constants and twiddle tables for ring dimension N = 2^logN.
  * psis[i] is the primitive 2N-th root used by the reference (modmath.py:61-68: smallest
  * generator g, psi = g^((q-1)/2N)); tables follow ntt.py:22-67.  Replaces the reference's

@@ -28,6 +28,8 @@ def _load():
     sig = {
         "lf_abi_version": (ctypes.c_int, []),
         "lf_last_error": (ctypes.c_char_p, []),
+        "lf_set_bconv_engine": (ctypes.c_int, [ctypes.c_int]),
+        "lf_get_bconv_engine": (ctypes.c_int, []),
         "lf_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _u32_host, _u32_host,
                                          ctypes.POINTER(ctypes.c_void_p)]),
         "lf_ctx_destroy": (ctypes.c_int, [ctypes.c_void_p]),

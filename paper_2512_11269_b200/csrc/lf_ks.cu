@@ -1181,11 +1181,16 @@ static int launch_bc_tc(const LfCtx* ctx, const BcArgs& A, int batch, cudaStream
 // counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches with at most 12
 // sources per group use the compile-time-K kernel.  With byte-split weight tables (k <= 15)
 // the conversion runs on the tensor cores (k_bconv_tc; LF_BC_TC=0 selects the IMAD kernel).
+static int g_bc_engine = -1;     // -1: not read yet; 1: tensor cores when tables allow; 0: IMAD
+static int bc_engine() {
+  if (g_bc_engine < 0) g_bc_engine = env_int("LF_BC_TC", 1) ? 1 : 0;
+  return g_bc_engine;
+}
+
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   if constexpr (L1 == 8 && L2 == 8) {
-    static const int use_tc = env_int("LF_BC_TC", 1);
-    bool tc = use_tc != 0;
+    bool tc = bc_engine() != 0;
     int kb = 0;
     for (int g = 0; g < A.ngroups && tc; ++g) {
       tc = A.g[g].B.w8 != nullptr;
@@ -1565,6 +1570,13 @@ static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
 }
 
 extern "C" {
+
+int lf_set_bconv_engine(int engine) {
+  if (engine != 0 && engine != 1) { lf_set_error("bconv engine %d (0: IMAD, 1: tensor cores)", engine); return 2; }
+  g_bc_engine = engine;
+  return 0;
+}
+int lf_get_bconv_engine(void) { return bc_engine(); }
 
 int lf_ctx_enable_keyswitch(lf_ctx* ctx, int n_main, int d) {
   if (!ctx) { lf_set_error("null context"); return 1; }
