@@ -10,9 +10,10 @@ the results copied back inside the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
-`--impl reference` times the reference algorithm on the host CPU cores instead (the CPU
-oracle `oracle/lf_oracle.py`, a restatement of limbforge ckks.keyswitch — the reference
-itself is pure Python and cannot travel to the GPU box), with one worker process per core.
+`--impl reference` times the reference itself on the host CPU cores instead: the unmodified
+`limbforge.ckks.keyswitch` (installed into baseline/_ref, which travels to the GPU box), one
+worker process per core; if baseline/_ref is missing it falls back to the CPU oracle
+`oracle/lf_oracle.py` (a restatement of the same function) and says so (`kind: "port"`).
 """
 
 import argparse
@@ -31,6 +32,7 @@ C2 = dict(N=65536, num_levels=35, d=4, seed=0, scale=2 ** 26)
 ROW_BYTES = 65536 * 4
 METRIC = "keyswitch ops/s"
 STAGES = ["modup_in", "modup_bconv", "ks_inner", "moddown_bconv", "moddown_out"]
+TRAFFIC_JSON = "r02_ncu_traffic.json"     # tools/ncu_traffic.py over a capture of this tree
 
 
 def algorithmic_rows(level=35, d=4, alpha=9):
@@ -41,8 +43,15 @@ def algorithmic_rows(level=35, d=4, alpha=9):
     return l1 + 2 * beta * ext + 2 * l1
 
 
+def key_rows(level=35, d=4, alpha=9):
+    """Evaluation-key rows one keyswitch reads: 2*beta*ext (shared by a relinearisation batch)."""
+    l1 = level + 1
+    return 2 * min(d, l1) * (l1 + alpha)
+
+
 def stage_rows(level=35, d=4, alpha=9):
-    """Algorithmic rows read+written by each fused kernel ('Kernels')."""
+    """Algorithmic rows read+written by each fused kernel ('Kernels'), per
+    keyswitch, the evaluation key charged per keyswitch (SURVEY §8d's definition)."""
     l1 = level + 1
     beta = min(d, l1)
     ext = l1 + alpha
@@ -122,6 +131,71 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_module():
+    """The unmodified reference package from baseline/_ref, or None when it is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "limbforge")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import limbforge.ckks  # noqa: F401
+        import limbforge.keys  # noqa: F401
+        import limbforge.params  # noqa: F401
+        import limbforge.poly  # noqa: F401
+        import limbforge
+        return limbforge
+    except Exception:
+        return None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _reference_setup(lf, level=35):
+    """C2 parameters, a relinearisation-shaped key with uniform rows (keyswitch cost is
+    data-independent) and warm NTT tables, all through the reference's own types."""
+    from limbforge.keys import EvalKey
+    from limbforge.ntt import ntt_tables
+    from limbforge.poly import Domain, RnsPolynomial, extended_ids, main_ids, prime_for_id
+    P = lf.params.gen_params(**C2)
+    ext = extended_ids(P, P.max_level)
+    rng = np.random.default_rng(7)
+
+    def rows(ids, r):
+        return np.stack([r.integers(0, prime_for_id(P, b), P.N, dtype=np.uint64) for b in ids])
+    evk = EvalKey("relin", tuple((RnsPolynomial(rows(ext, rng), Domain.EVAL, ext),
+                                  RnsPolynomial(rows(ext, rng), Domain.EVAL, ext)) for _ in range(P.ks.d)))
+    for b in ext:
+        ntt_tables(P.N, prime_for_id(P, b))
+    ids = main_ids(level)
+    mk = lambda seed: RnsPolynomial(rows(ids, np.random.default_rng(seed)), Domain.EVAL, ids)
+    return P, evk, mk
+
+
+def cpu_reference_keyswitch_sample(n_ops=2, level=35):
+    """Time the reference's own limbforge.ckks.keyswitch on one core (bounded sample)."""
+    lf = reference_module()
+    if lf is None:
+        return None
+    P, evk, mk = _reference_setup(lf, level)
+    xs = [mk(1000 + i) for i in range(n_ops)]
+    t0 = time.perf_counter()
+    for x in xs:
+        lf.ckks.keyswitch(x, evk, P)
+    dt = time.perf_counter() - t0
+    return n_ops / dt, dt
+
+
 def cpu_oracle_keyswitch_sample(n_ops=2, level=35):
     """Time the CPU oracle (restatement of limbforge ckks.keyswitch) on a bounded sample."""
     from oracle import lf_oracle as O
@@ -146,6 +220,11 @@ _REF_STATE = {}
 
 
 def _ref_worker_init():
+    lf = reference_module()
+    if lf is not None:
+        P, evk, mk = _reference_setup(lf)
+        _REF_STATE.update(kind="reference", run=lambda seed: lf.ckks.keyswitch(mk(seed), evk, P))
+        return
     from oracle import lf_oracle as O
     P = O.gen_params(**C2)
     ext = P.ext_ids(P.L)
@@ -154,25 +233,27 @@ def _ref_worker_init():
                                for _ in range(P.d)])
     for q in P.main + P.special:
         O.twiddles(P.N, q)
-    _REF_STATE.update(P=P, evk=evk, O=O)
+    _REF_STATE.update(kind="port", run=lambda seed: O.keyswitch(
+        P, O.sample_uniform(P, np.random.default_rng(seed), P.main_ids(P.L)), evk))
 
 
 def _ref_worker_ks(seed):
-    O, P, evk = _REF_STATE["O"], _REF_STATE["P"], _REF_STATE["evk"]
-    x = O.sample_uniform(P, np.random.default_rng(seed), P.main_ids(P.L))
     t0 = time.perf_counter()
-    O.keyswitch(P, x, evk)
+    _REF_STATE["run"](seed)
     return time.perf_counter() - t0
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (CPU oracle) on all host cores.  The key and
-    twiddle tables are built once in the parent and shared copy-on-write with the workers."""
+    """--impl reference: the reference's own limbforge.ckks.keyswitch (baseline/_ref) on all
+    host cores (the oracle port if the reference is not installed).  The key and twiddle tables
+    are built once in the parent and shared copy-on-write with the workers."""
     if rank != 0:
         return
     import multiprocessing as mp
     cores = min(os.cpu_count() or 1, 64)
     _ref_worker_init()
+    kind = _REF_STATE["kind"]
+    what = "limbforge.ckks.keyswitch (baseline/_ref)" if kind == "reference" else "oracle/lf_oracle.py"
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         for w in range(args.warmup):
@@ -190,8 +271,9 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": "C2 full-level hybrid keyswitch, N=2^16, L=35, dnum=4, alpha=9",
                    "level": 35, "batch_per_step": cores, "sample": "one keyswitch per core per step"},
-        "cpu_baseline": {"value": value, "unit": "ops/s", "cores": cores, "kind": "port",
-                         "sample": f"{ops} C2 keyswitches, {cores} worker processes (oracle/lf_oracle.py)"},
+        "cpu_baseline": {"value": value, "unit": "ops/s", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(),
+                         "sample": f"{ops} C2 keyswitches, {cores} worker processes ({what})"},
         "e2e": {"value": value, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -519,8 +601,14 @@ def run_ours(args, rank, world):
         stage += np.array(fused.keyswitch_batch_profiled(params, level, xs[i % nsets], rlk, out, ws))
     stage /= 3
     rows = stage_rows(level)
+    krows = key_rows(level)
+
+    def batch_rows(n):          # the shared relinearisation key is read once per batch
+        return rows[n] * Bsz - (krows * (Bsz - 1) if n == "ks_inner" else 0)
     stage_info = {n: {"ms": float(t), "share": float(t / stage.sum()),
-                      "gbs": rows[n] * ROW_BYTES * Bsz / (t / 1e3) / 1e9} for n, t in zip(STAGES, stage)}
+                      "gbs": batch_rows(n) * ROW_BYTES / (t / 1e3) / 1e9,
+                      "gbs_key_per_op": rows[n] * ROW_BYTES * Bsz / (t / 1e3) / 1e9}
+                  for n, t in zip(STAGES, stage)}
     top = max(STAGES, key=lambda n: stage_info[n]["ms"])
     peaks = {}
     try:
@@ -534,10 +622,11 @@ def run_ours(args, rank, world):
     traffic = None            # ncu dram bytes of the same kernel, per launch (profiles/, committed)
     pipes = None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)))
         if top in tr and tr[top].get("batch", 8) == Bsz and level == 35:
             traffic = tr[top]["bytes_per_launch"]
-            pipes = {k: tr[top].get(k) for k in ("fmaheavy_pipe_pct", "issue_active_pct", "l1tex_pct", "dram_pct")}
+            pipes = {k: tr[top].get(k) for k in ("fmaheavy_pipe_pct", "issue_active_pct", "l1tex_pct",
+                                                 "dram_pct", "kernel", "tree")}
     except Exception:
         pass
 
@@ -600,9 +689,15 @@ def run_ours(args, rank, world):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, dt = cpu_oracle_keyswitch_sample(2, level)
-        cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "port",
-               "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
+        r = cpu_reference_keyswitch_sample(2, level)
+        if r is not None:
+            v, dt = r
+            cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "reference", "cpu_model": cpu_model(),
+                   "sample": f"2 C2 full-level keyswitches, limbforge.ckks.keyswitch (baseline/_ref) on 1 core ({dt:.1f} s)"}
+        else:
+            v, dt = cpu_oracle_keyswitch_sample(2, level)
+            cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+                   "sample": f"2 C2 full-level keyswitches, oracle/lf_oracle.py on 1 core ({dt:.1f} s)"}
 
     ntt = ntt_throughput(params, dev)
     sweep = batch_sweep(params, level, rlk, dev) if rank == 0 else None
@@ -630,13 +725,23 @@ def run_ours(args, rank, world):
                        "l2": "256 MB flush between timed steps; inputs cycled over 3 batches"},
             "keyswitch_us": ms / args.steps / Bsz * 1e3,
             "keyswitch_hbm": {"algorithmic_bytes": ks_bytes, "achieved_gbs": ks_bytes * value / world / 1e9,
-                              "peak_gbs": hbm_peak, "frac": ks_bytes * value / world / 1e9 / hbm_peak},
+                              "peak_gbs": hbm_peak, "frac": ks_bytes * value / world / 1e9 / hbm_peak,
+                              "key": "charged per keyswitch (SURVEY 8d: 468 rows at C2)"},
+            "keyswitch_hbm_batch": {
+                "algorithmic_bytes_per_batch": (algorithmic_rows(level) * Bsz - key_rows(level) * (Bsz - 1)) * ROW_BYTES,
+                "achieved_gbs": (algorithmic_rows(level) * Bsz - key_rows(level) * (Bsz - 1)) * ROW_BYTES
+                                / (ms / args.steps / 1e3) / 1e9,
+                "peak_gbs": hbm_peak,
+                "frac": (algorithmic_rows(level) * Bsz - key_rows(level) * (Bsz - 1)) * ROW_BYTES
+                        / (ms / args.steps / 1e3) / 1e9 / hbm_peak,
+                "key": "the shared relinearisation key read once per batch"},
             "roofline": {"kernel": top, "bound": "hbm", "achieved": achieved_top, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": rows[top] * ROW_BYTES * Bsz,
+                         "algorithmic_bytes_per_launch": batch_rows(top) * ROW_BYTES,
                          "ncu_pipes": pipes,
                          "peak_source": peak_src,
-                         "note": "algorithmic bytes / CUDA-event time of the launch; traffic = ncu dram read+write of the same launch (profiles/r01_ncu_traffic.json)"},
+                         "binding_resource": "FMA-heavy integer pipe (NTT Shoup products), not HBM: see ncu_pipes",
+                         "note": f"algorithmic bytes / CUDA-event time of the launch; traffic = ncu dram read+write of the same launch (profiles/{TRAFFIC_JSON})"},
             "stages": stage_info,
             "gpu_launches": 5 * args.steps,
             "e2e": {"value": e2e_value, "unit": "ops/s",

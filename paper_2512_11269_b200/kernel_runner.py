@@ -99,7 +99,9 @@ class KernelRunner:
             stage = torch.empty((len(slots), N), dtype=torch.int32, device="cuda")
             if rd:
                 from .serial import _upload_rows
-                up = _upload_rows(np.stack([np.asarray(read_row(plan.operand_table[i]), dtype=np.uint64)
+                # copy each row as it is returned: the Executor hands out compressed operands
+                # expanded into a small ring of reused buffers (runtime.py read_pooled)
+                up = _upload_rows(np.stack([np.array(read_row(plan.operand_table[i]), dtype=np.uint64, copy=True)
                                             for i in rd]))
                 idx = {s: j for j, s in enumerate(slots)}
                 stage[[idx[i] for i in rd]] = up

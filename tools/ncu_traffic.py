@@ -1,50 +1,67 @@
-"""Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the keyswitch
-kernels from one `ncu --set full` capture of `tools/profile_ks.py 8 1`, written as JSON for
-bench.py's roofline.traffic (profiles/r01_ncu_traffic.json)."""
+"""Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) and pipe utilisation
+of the five keyswitch kernels, from a light ncu capture of `tools/profile_ks.py 32 2`, written
+as JSON for bench.py's roofline.traffic / ncu_pipes (profiles/r02_ncu_traffic.json).
+
+Capture (on the GPU box; the csv is small, no .ncu-rep needed):
+    ncu --clock-control none --metrics $(python tools/ncu_traffic.py --metrics) \
+        -k regex:"k_modup_in|k_bconv|k_ks_inner|k_moddown_out" -s 5 -c 5 --csv \
+        python tools/profile_ks.py 32 2 > gpurun_out/traffic.csv
+Summarise:
+    python tools/ncu_traffic.py gpurun_out/traffic.csv profiles/r02_ncu_traffic.json --batch=32 --tree=<git sha>
+"""
 import csv
 import json
-import subprocess
 import sys
 
-STAGE_OF = [("k_modup_in", "modup_in"), ("k_ks_inner", "ks_inner"), ("k_moddown_out", "moddown_out")]
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "l1tex__throughput.avg.pct_of_peak_sustained_active",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
 
 
-def main(reps, out, batch=8):
-    res = {}
-    for rep in reps:
-        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(txt.splitlines()))
-        h, units = rows[0], rows[1]
-        bc = 0
-        for r in rows[2:]:
-            name = r[h.index("Kernel Name")]
-            tot = 0.0
-            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                u = units[h.index(m)]
-                f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-                tot += float(r[h.index(m)]) * f
-            st = None
-            if "k_bconv_colpass" in name:
-                st = "modup_bconv" if bc == 0 else "moddown_bconv"
-                bc += 1
-            for k, s in STAGE_OF:
-                if name.startswith("void " + k) or name.startswith(k):
-                    st = s
-            if st and st not in res:
-                def metric(m):
-                    return float(r[h.index(m)]) if m in h and r[h.index(m)] not in ("", "n/a") else None
-                res[st] = {"bytes_per_launch": tot, "report": rep, "launch": f"batch of {batch} C2 keyswitches", "batch": batch,
-                           "fmaheavy_pipe_pct": metric("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
-                           "issue_active_pct": metric("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                           "l1tex_pct": metric("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                           "dram_pct": metric("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+def stage_of(name, nbconv):
+    if "k_bconv" in name:
+        return "modup_bconv" if nbconv == 0 else "moddown_bconv"
+    for k, s in (("k_modup_in", "modup_in"), ("k_ks_inner", "ks_inner"), ("k_moddown_out", "moddown_out")):
+        if k in name:
+            return s
+    return None
+
+
+def main(path, out, batch, tree):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    h = rows[0]
+    iid, ik, im, iu, iv = (h.index(c) for c in ("ID", "Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
+    launches = {}
+    for r in rows[1:]:
+        d = launches.setdefault(r[iid], {"name": r[ik]})
+        v = float(r[iv].replace(",", ""))
+        d[r[im]] = v * UNIT.get(r[iu], 1.0)
+    res, nb = {}, 0
+    for lid in sorted(launches, key=int):
+        d = launches[lid]
+        st = stage_of(d["name"], nb)
+        if "k_bconv" in d["name"]:
+            nb += 1
+        if st is None or st in res:
+            continue
+        res[st] = {"kernel": d["name"].split("(")[0].replace("void ", ""),
+                   "bytes_per_launch": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
+                   "time_us_ncu": d.get("gpu__time_duration.sum"),
+                   "launch": f"batch of {batch} C2 keyswitches", "batch": batch, "tree": tree,
+                   "fmaheavy_pipe_pct": d.get(METRICS[3]), "issue_active_pct": d.get(METRICS[4]),
+                   "l1tex_pct": d.get(METRICS[5]), "dram_pct": d.get(METRICS[6])}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    batch = 8
-    if args and args[0].startswith("--batch="):
-        batch = int(args.pop(0).split("=")[1])
-    main(args[:-1], args[-1], batch)
+    if args == ["--metrics"]:
+        print(",".join(METRICS))
+        sys.exit(0)
+    opts = {a.split("=")[0]: a.split("=", 1)[1] for a in args if a.startswith("--")}
+    pos = [a for a in args if not a.startswith("--")]
+    main(pos[0], pos[1], int(opts.get("--batch", 32)), opts.get("--tree"))
