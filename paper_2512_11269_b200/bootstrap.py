@@ -263,6 +263,10 @@ def cheb_divmod(c: np.ndarray, G: int):
     return q, r
 
 
+TWICE_MIN_SCALE = 2 ** 20      # lowest declared scale the free Chebyshev doubling may leave (default
+                               # degree 31: T_16 at ~2^37, untouched)
+
+
 @dataclass(frozen=True)
 class BootConfig:
     cts_levels: int = 4
@@ -433,8 +437,13 @@ class Bootstrapper:
         T = {1: u}
         g = self.cfg.baby
 
-        def twice(x):                           # 2x: the same residues at half the scale
-            return be.with_scale(x, Fraction(x.scale) / 2)
+        def twice(x):
+            # 2x: the same residues at half the declared scale (free) while the scale stays
+            # >= 2^20 (advisor budget: 2^k - 1 < log2 s - 20); past that (high cheb_degree: T_2^k sits at
+            # s / 2^(2^k - 1)) an exact addition keeps the scale
+            if Fraction(x.scale) / 2 >= TWICE_MIN_SCALE:
+                return be.with_scale(x, Fraction(x.scale) / 2)
+            return be.add(x, x)
 
         def double(k):                          # T_2k = 2 T_k^2 - 1
             x = twice(self._mul2(T[k], T[k]))
@@ -774,7 +783,7 @@ class GpuBackend:
         out = torch.empty((n, 2, ext, self.params.N), dtype=torch.int32, device="cuda")
         gs = [galois_element_of(self.params.N, s) for s in steps]
         keys = self._rot_keys(steps)
-        karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
+        karr = (ctypes.c_void_p * n)(*[ctx.check_evk(k).data_ptr() for k in keys])
         c = ct_block(ct)
         fn = lib.lf_rotate_hoisted_ext_pk if self.permuted_keys else lib.lf_rotate_hoisted_ext
         _native.check(fn(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
@@ -811,7 +820,7 @@ class GpuBackend:
                 pt0 = pt
         parr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         keys = self._rot_keys(rot)
-        karr = (ctypes.c_void_p * len(rot))(*[k.data.data_ptr() for k in keys])
+        karr = (ctypes.c_void_p * len(rot))(*[ctx.check_evk(k).data_ptr() for k in keys])
         gs = [galois_element_of(N, b) for b in rot]
         ws = torch.empty(lib.lf_rotate_hoisted_workspace_bytes(ctx.handle, level, 1) // 4,
                          dtype=torch.int32, device="cuda")

@@ -33,8 +33,14 @@ def stream_handle():
 
 
 def dptr(t: torch.Tensor):
+    """Raw device pointer for the C ABI: the kernels index rows densely, so a strided view or
+    a tensor on another GPU than the current one is rejected instead of read out of bounds."""
     if not t.is_cuda:
         raise _native.NativeError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise _native.NativeError(f"expected a contiguous tensor (shape {tuple(t.shape)}, strides {t.stride()})")
+    if t.device.index != torch.cuda.current_device():
+        raise _native.NativeError(f"tensor on cuda:{t.device.index}, current device cuda:{torch.cuda.current_device()}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -57,12 +63,36 @@ class DeviceContext:
         self.handle = h
         self._blobs = {}
         self._pidx = {}
+        self._ws = {}
         _native.check(self._lib.lf_ctx_enable_keyswitch(h, self.L + 1, params.ks.d),
                       "lf_ctx_enable_keyswitch")
 
     def ks_workspace(self, level: int, batch: int = 1) -> torch.Tensor:
         nbytes = self._lib.lf_ks_workspace_bytes(self.handle, level, batch)
         return torch.empty(nbytes // 4, dtype=torch.int32, device="cuda")
+
+    def ks_workspace_cached(self, level: int, batch: int = 1) -> torch.Tensor:
+        """A keyswitch workspace reused by every call on the current stream (kernels of one
+        stream run in order, so consecutive calls cannot overlap in it); grown on demand."""
+        need = self._lib.lf_ks_workspace_bytes(self.handle, level, batch) // 4
+        if torch.cuda.is_current_stream_capturing():      # a captured graph keeps its own
+            return torch.empty(need, dtype=torch.int32, device="cuda")
+        key = torch.cuda.current_stream().cuda_stream
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.int32, device="cuda")
+            self._ws[key] = ws
+        return ws[:need]
+
+    def check_evk(self, evk):
+        """The fused entry points read an evaluation key as ONE dense (d, 2, L+1+alpha, N)
+        tensor (keys.EvalKey) on this context's device."""
+        t = getattr(evk, "data", None)
+        want = (self.params.ks.d, 2, self.L + 1 + self.alpha, self.N)
+        if not isinstance(t, torch.Tensor) or tuple(t.shape) != want or t.dtype != torch.int32:
+            raise _native.NativeError(f"evaluation key must be an int32 tensor of shape {want}, got "
+                                      f"{getattr(t, 'shape', None)} {getattr(t, 'dtype', None)}")
+        return t
 
     def rescale_workspace(self, level: int, batch: int = 1) -> torch.Tensor:
         nbytes = self._lib.lf_rescale_workspace_bytes(self.handle, level, batch)
@@ -160,8 +190,12 @@ _CTX = {}
 
 
 def get_context(params: CkksParams) -> DeviceContext:
-    ctx = _CTX.get(params)
+    """One context per (parameter set, device): tables and plans live on the device that was
+    current when the context was built."""
+    require_cuda()
+    key = (params, torch.cuda.current_device())
+    ctx = _CTX.get(key)
     if ctx is None:
         ctx = DeviceContext(params)
-        _CTX[params] = ctx
+        _CTX[key] = ctx
     return ctx

@@ -23,6 +23,7 @@ The compiled pipeline (pipeline.py / runtime.py Executor) instead executes kerne
         result = rt.Executor(compiled, ...).run(...)        # every kernel plan on the GPU
 """
 
+import weakref
 from fractions import Fraction
 
 from . import ckks as C
@@ -57,10 +58,18 @@ def as_key(k):
     if k is None or isinstance(k, EvalKey):
         return k
     got = _KEYS.get(id(k))
-    if got is None or got[0] is not k:
-        got = (k, EvalKey.from_reference(k))
+    if got is None or got[0]() is not k:
+        got = (weakref.ref(k), EvalKey.from_reference(k))
         _KEYS[id(k)] = got
+        weakref.finalize(k, _KEYS.pop, id(k), None)     # device copy freed with the reference key
     return got[1]
+
+
+def clear_cache():
+    """Drop every cached device key and parameter conversion (HBM is released once the
+    evaluator holds no other reference to the device keys)."""
+    _KEYS.clear()
+    _PARAMS.clear()
 
 
 def hom_add(ct1, ct2, params):
@@ -103,6 +112,7 @@ class Installed:
         for name, fn in self.saved.items():
             setattr(self.module, name, fn)
         self.saved = {}
+        clear_cache()
 
     def __enter__(self):
         return self

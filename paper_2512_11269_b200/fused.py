@@ -29,10 +29,10 @@ def _pair(out: torch.Tensor, ids):
 def keyswitch(params, x: RnsPolynomial, evk):
     ctx = get_context(params)
     level = len(x.basis_ids) - 1
-    ws = ctx.ks_workspace(level)
+    ws = ctx.ks_workspace_cached(level)
     out = torch.empty((2, level + 1, params.N), dtype=torch.int32, device=x.limbs.device)
     xl = x.limbs.contiguous()
-    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xl), 0, dptr(evk.data), 0,
+    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xl), 0, dptr(ctx.check_evk(evk)), 0,
                                              dptr(out), 0, 1, dptr(ws), stream_handle()),
                   "lf_keyswitch")
     return _pair(out, main_ids(level))
@@ -41,10 +41,10 @@ def keyswitch(params, x: RnsPolynomial, evk):
 def hom_mul(params, ct1, ct2, rlk):
     ctx = get_context(params)
     level = ct1.level
-    ws = ctx.ks_workspace(level)
+    ws = ctx.ks_workspace_cached(level)
     c1, c2 = ct_block(ct1), ct_block(ct2)
     out = torch.empty_like(c1)
-    _native.check(_native.lib().lf_hom_mul(ctx.handle, level, dptr(c1), dptr(c2), 0, dptr(rlk.data),
+    _native.check(_native.lib().lf_hom_mul(ctx.handle, level, dptr(c1), dptr(c2), 0, dptr(ctx.check_evk(rlk)),
                                            dptr(out), 0, 1, dptr(ws), stream_handle()), "lf_hom_mul")
     return _pair(out, main_ids(level))
 
@@ -55,11 +55,11 @@ def hom_mul_rescale(params, ct1, ct2, rlk, ndrop: int = 1):
     ct1.level - ndrop."""
     ctx = get_context(params)
     level = ct1.level
-    ws = ctx.ks_workspace(level)
+    ws = ctx.ks_workspace_cached(level)
     c1, c2 = ct_block(ct1), ct_block(ct2)
     out = torch.empty((2, max(level + 1 - ndrop, 1), params.N), dtype=torch.int32, device=c1.device)
     _native.check(_native.lib().lf_hom_mul_rescale(ctx.handle, level, ndrop, dptr(c1), dptr(c2), 0,
-                                                   dptr(rlk.data), dptr(out), 0, 1, dptr(ws),
+                                                   dptr(ctx.check_evk(rlk)), dptr(out), 0, 1, dptr(ws),
                                                    stream_handle()), "lf_hom_mul_rescale")
     return _pair(out, main_ids(level - ndrop))
 
@@ -67,10 +67,10 @@ def hom_mul_rescale(params, ct1, ct2, rlk, ndrop: int = 1):
 def rotate(params, ct, g: int, key):
     ctx = get_context(params)
     level = ct.level
-    ws = ctx.ks_workspace(level)
+    ws = ctx.ks_workspace_cached(level)
     c = ct_block(ct)
     out = torch.empty_like(c)
-    _native.check(_native.lib().lf_rotate(ctx.handle, level, dptr(c), 0, g, dptr(key.data), 0,
+    _native.check(_native.lib().lf_rotate(ctx.handle, level, dptr(c), 0, g, dptr(ctx.check_evk(key)), 0,
                                           dptr(out), 0, 1, dptr(ws), stream_handle()), "lf_rotate")
     return _pair(out, main_ids(level))
 
@@ -86,7 +86,7 @@ def rotate_hoisted(params, ct, gs, keys):
                      dtype=torch.int32, device="cuda")
     c = ct_block(ct)
     out = torch.empty((n, 2, level + 1, params.N), dtype=torch.int32, device=c.device)
-    karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
+    karr = (ctypes.c_void_p * n)(*[ctx.check_evk(k).data_ptr() for k in keys])
     _native.check(lib.lf_rotate_hoisted(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
                                         dptr(out), out[0].numel(), dptr(ws), stream_handle()),
                   "lf_rotate_hoisted")
@@ -115,7 +115,7 @@ def rotate_batch(params, level: int, cts: torch.Tensor, gs, keys, permuted: bool
     lib = _native.lib()
     ws = ctx.ks_workspace(level, min(n, 64))
     out = torch.empty_like(cts)
-    karr = (ctypes.c_void_p * n)(*[k.data.data_ptr() for k in keys])
+    karr = (ctypes.c_void_p * n)(*[ctx.check_evk(k).data_ptr() for k in keys])
     fn = lib.lf_rotate_batch_pk if permuted else lib.lf_rotate_batch
     _native.check(fn(ctx.handle, level, dptr(cts), cts[0].numel(), n, _native.u32_array(gs),
                      karr, dptr(out), out[0].numel(), dptr(ws), stream_handle()),
@@ -151,7 +151,7 @@ def decompose(params, x: RnsPolynomial):
     level = len(x.basis_ids) - 1
     ext = extended_ids(params, level)
     beta = min(params.ks.d, level + 1)
-    ws = ctx.ks_workspace(level)
+    ws = ctx.ks_workspace_cached(level)
     pieces = torch.empty((beta, len(ext), params.N), dtype=torch.int32, device=x.limbs.device)
     xl = x.limbs.contiguous()
     _native.check(_native.lib().lf_ks_decompose(ctx.handle, level, dptr(xl), dptr(pieces), dptr(ws),
@@ -170,7 +170,7 @@ def keyswitch_batch(params, level: int, xs: torch.Tensor, evk, out: torch.Tensor
         ws = ctx.ks_workspace(level, B)
     if out is None:
         out = torch.empty((B, 2, level + 1, params.N), dtype=torch.int32, device=xs.device)
-    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xs), xs[0].numel(), dptr(evk.data), 0,
+    _native.check(_native.lib().lf_keyswitch(ctx.handle, level, dptr(xs), xs[0].numel(), dptr(ctx.check_evk(evk)), 0,
                                              dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
                   "lf_keyswitch")
     return out
@@ -184,6 +184,6 @@ def keyswitch_batch_profiled(params, level: int, xs: torch.Tensor, evk, out: tor
     ctx = get_context(params)
     ms = (ctypes.c_float * 5)()
     _native.check(_native.lib().lf_keyswitch_profiled(
-        ctx.handle, level, dptr(xs), xs[0].numel(), dptr(evk.data), 0, dptr(out), out[0].numel(),
+        ctx.handle, level, dptr(xs), xs[0].numel(), dptr(ctx.check_evk(evk)), 0, dptr(out), out[0].numel(),
         xs.shape[0], dptr(ws), stream_handle(), ms), "lf_keyswitch_profiled")
     return list(ms)

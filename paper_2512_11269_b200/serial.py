@@ -62,7 +62,31 @@ def ids_for_primes(params, primes) -> tuple:
     from .context import SPECIAL_BASE
     lookup = {q: i for i, q in enumerate(params.rns_basis)}
     lookup.update({q: SPECIAL_BASE + j for j, q in enumerate(params.special_basis)})
+    unknown = [q for q in primes if q not in lookup]
+    if unknown:
+        raise ValueError(f"LFHE blob primes {unknown[:3]} are not in this parameter set's basis")
     return tuple(lookup[q] for q in primes)
+
+
+def _check_blob(params, N, primes, expected_ids=None, what="blob"):
+    """Reject blobs built for other parameters before anything reaches the device: the fused
+    kernels index device rows with the context's N, level and digit counts, so a foreign
+    shape would be read out of bounds instead of failing like the reference's numpy code."""
+    if N != params.N:
+        raise ValueError(f"LFHE {what}: N={N} but the parameters have N={params.N}")
+    if len(set(primes)) != len(primes):
+        raise ValueError(f"LFHE {what}: repeated primes in the header")
+    ids = ids_for_primes(params, primes)
+    if expected_ids is not None and tuple(ids) != tuple(expected_ids):
+        raise ValueError(f"LFHE {what}: basis {ids[:4]}... is not the expected {tuple(expected_ids)[:4]}...")
+    return ids
+
+
+def _check_residues(rows, primes, what):
+    """Every residue below its prime (lf_rows_from_u64 narrows u64 -> u32 without a check)."""
+    q = np.asarray(primes, dtype=np.uint64)
+    if (rows.reshape(-1, len(primes), rows.shape[-1]) >= q[None, :, None]).any():
+        raise ValueError(f"LFHE {what}: residue not below its prime")
 
 
 def primes_for_ids(params, ids) -> list:
@@ -120,7 +144,9 @@ def poly_to_bytes(poly, params, scale=0.0, level=None, kind=KIND_POLY) -> bytes:
 def poly_from_bytes(data, params):
     from .poly import Domain, RnsPolynomial
     kind, N, primes, level, scale, domain, off = parse_header(data)
+    _check_blob(params, N, primes, what="polynomial")
     rows, off = rows_view(data, off, len(primes), N)
+    _check_residues(rows, primes, "polynomial")
     poly = RnsPolynomial(_upload_rows(rows), Domain.COEFF if domain == 0 else Domain.EVAL,
                          ids_for_primes(params, primes))
     return kind, poly, level, scale, off
@@ -132,9 +158,12 @@ def plaintext_to_bytes(pt, params) -> bytes:
 
 def plaintext_from_bytes(data, params):
     from .encoding import Plaintext
+    from .poly import main_ids
+    if detect_kind(data) != KIND_PLAINTEXT:
+        raise ValueError(f"LFHE kind {detect_kind(data)} is not a plaintext")
     kind, poly, level, scale, _ = poly_from_bytes(data, params)
-    if kind != KIND_PLAINTEXT:
-        raise ValueError(f"LFHE kind {kind} is not a plaintext")
+    if tuple(poly.basis_ids) != main_ids(level):
+        raise ValueError(f"LFHE plaintext: basis does not match level {level}")
     return Plaintext(poly=poly, scale=Fraction(scale), level=level)
 
 
@@ -150,7 +179,12 @@ def ciphertext_from_bytes(data, params):
     kind, N, primes, level, scale, domain, off = parse_header(data)
     if kind != KIND_CIPHERTEXT:
         raise ValueError(f"LFHE kind {kind} is not a ciphertext")
+    from .poly import main_ids
+    if level > params.max_level:
+        raise ValueError(f"LFHE ciphertext: level {level} above the parameters' {params.max_level}")
+    _check_blob(params, N, primes, main_ids(level), "ciphertext")
     rows, _ = rows_view(data, off, 2 * len(primes), N)         # b rows then a rows, one upload
+    _check_residues(rows, primes, "ciphertext")
     dev = _upload_rows(rows)
     from .poly import Domain
     dom = Domain.COEFF if domain == 0 else Domain.EVAL
@@ -178,9 +212,16 @@ def evalkey_from_bytes(data, params):
     kind, N, primes, _, _, _, off = parse_header(data)
     if kind != KIND_EVALKEY:
         raise ValueError(f"LFHE kind {kind} is not an evaluation key")
+    from .poly import extended_ids
+    _check_blob(params, N, primes, extended_ids(params, params.max_level), "evaluation key")
     tag, rot, ndig = struct.unpack_from("<BIH", data, off)
     off += struct.calcsize("<BIH")
+    if ndig != params.ks.d:
+        raise ValueError(f"LFHE evaluation key: {ndig} digits but the parameters use d={params.ks.d}")
+    if tag not in (0, 1):
+        raise ValueError(f"LFHE evaluation key: purpose tag {tag}")
     rows, _ = rows_view(data, off, ndig * 2 * len(primes), N)
+    _check_residues(rows, primes, "evaluation key")
     dev = _upload_rows(rows).view(ndig, 2, len(primes), N)
     purpose = "relin" if tag == 0 else ("rot", rot)
     return EvalKey(purpose, dev, ids_for_primes(params, primes))
@@ -196,9 +237,44 @@ def secret_from_bytes(data, params):
     from .encoding import signed_to_eval
     from .keys import SecretKey
     from .poly import extended_ids
-    kind, N, _, _, _, _, off = parse_header(data)
+    kind, N, primes, _, _, _, off = parse_header(data)
     if kind != KIND_SECRET:
         raise ValueError(f"LFHE kind {kind} is not a secret key")
+    _check_blob(params, N, primes, what="secret key")
     coeffs = np.frombuffer(data, dtype="<i1", count=N, offset=off).copy()
     s_eval = signed_to_eval(coeffs.astype(np.int64), params, extended_ids(params, params.max_level))
     return SecretKey(coeffs=coeffs, s_eval=s_eval)
+
+
+def compressed_to_bytes(cp, params) -> bytes:
+    """serial.py:144-151: header over the main basis of cp.level, (stride, unique count), then
+    the unique-value rows (u64)."""
+    head = pack_header(KIND_COMPRESSED, params.N, params.rns_basis[: cp.level + 1], cp.level, cp.scale, 1)
+    return head + struct.pack("<II", cp.descriptor.stride, cp.descriptor.unique_count) + \
+        _download_rows(cp.unique)
+
+
+def compressed_from_bytes(data, params):
+    """serial.py:154-166, the unique rows straight into HBM (compress.CompressedPlaintext)."""
+    from .compress import CompressedPlaintext, CompressionDescriptor
+    from .poly import main_ids
+    kind, N, primes, level, scale, _, off = parse_header(data)
+    if kind != KIND_COMPRESSED:
+        raise ValueError(f"LFHE kind {kind} is not a compressed plaintext")
+    _check_blob(params, N, primes, main_ids(level), "compressed plaintext")
+    stride, unique = struct.unpack_from("<II", data, off)
+    off += struct.calcsize("<II")
+    desc = CompressionDescriptor.for_params(params, stride)
+    if desc.unique_count != unique:
+        raise ValueError(f"LFHE compressed plaintext: {unique} unique values, stride {stride} implies "
+                         f"{desc.unique_count}")
+    rows = np.frombuffer(data, dtype="<u8", count=len(primes) * unique, offset=off).reshape(len(primes), unique)
+    _check_residues(rows, primes, "compressed plaintext")
+    return CompressedPlaintext(unique=_upload_rows(rows), descriptor=desc, scale=Fraction(scale), level=level)
+
+
+def load_plaintext_auto(data, params):
+    """serial.py:169-174: dense or compressed plaintext, dispatched on the header's kind."""
+    if detect_kind(data) == KIND_COMPRESSED:
+        return compressed_from_bytes(data, params)
+    return plaintext_from_bytes(data, params)

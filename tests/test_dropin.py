@@ -55,3 +55,26 @@ def test_install_runner_swaps_kernel_runner():
     with dropin.install_runner(m):
         assert m.KernelRunner is dropin.KernelRunner
     assert m.KernelRunner == "orig"
+
+
+def test_key_cache_is_weak_and_cleared_on_restore(monkeypatch):
+    """Device copies of reference keys are evicted when the reference key dies and on
+    restore() (no HBM leak across long-running evaluators)."""
+    import gc
+
+    class RefKey:                        # stands in for a reference EvalKey (weak-referenceable)
+        pass
+
+    monkeypatch.setattr(dropin.EvalKey, "from_reference", staticmethod(lambda k: ("device", id(k))))
+    k = RefKey()
+    dev = dropin.as_key(k)
+    assert dropin.as_key(k) is dev and id(k) in dropin._KEYS
+    kid = id(k)
+    del k
+    gc.collect()
+    assert kid not in dropin._KEYS
+    k2 = RefKey()
+    dropin.as_key(k2)
+    m = _fake_evaluate_module()
+    dropin.install(m).restore()
+    assert not dropin._KEYS

@@ -78,3 +78,53 @@ def test_device_roundtrip_and_parity(blobs, golden_params):
     # loaded objects compute: rotate with the loaded key, decrypt with the loaded secret
     dec = B.decrypt(B.hom_rotate(ct2, 1, r2, p), sk2, p)
     assert np.abs(dec - np.roll(v, -1)).max() < 0.05
+
+
+def test_foreign_blobs_rejected_before_upload(blobs, golden_params):
+    """Blobs for other parameters fail on the host with ValueError, never reach the device
+    (the fused kernels would index them with this context's shapes)."""
+    from paper_2512_11269_b200.params import gen_params
+    p = gen_params(**golden_params["small"]["kwargs"])
+    other_n = gen_params(512, 4, d=3, seed=3)
+    other_d = gen_params(256, 4, d=2, seed=3)
+    with pytest.raises(ValueError, match="N="):
+        S.ciphertext_from_bytes(blobs["ciphertext"], other_n)
+    with pytest.raises(ValueError):
+        S.evalkey_from_bytes(blobs["relin"], other_d)
+    with pytest.raises(ValueError, match="not in this parameter set"):
+        S.plaintext_from_bytes(blobs["plaintext"], gen_params(256, 4, d=3, seed=3, scale=2 ** 24))
+    with pytest.raises(ValueError, match="is not a ciphertext"):
+        S.ciphertext_from_bytes(blobs["plaintext"], p)
+    # a residue >= its prime
+    kind, N, primes, level, scale, domain, off = S.parse_header(blobs["ciphertext"])
+    bad = bytearray(blobs["ciphertext"])
+    bad[off: off + 8] = np.array([primes[0]], dtype="<u8").tobytes()
+    with pytest.raises(ValueError, match="residue"):
+        S.ciphertext_from_bytes(bytes(bad), p)
+    # a ciphertext header whose primes are not main 0..level
+    hdr = S.pack_header(S.KIND_CIPHERTEXT, N, primes[:3], 3, scale, domain)
+    with pytest.raises(ValueError, match="basis"):
+        S.ciphertext_from_bytes(hdr + blobs["ciphertext"][off:], p)
+
+
+def test_compressed_blob_layout(blobs, golden_params):
+    kind, N, primes, level, scale, domain, off = S.parse_header(blobs["compressed"])
+    assert kind == S.KIND_COMPRESSED and level == 3 and len(primes) == 4
+    assert S.detect_kind(blobs["compressed"]) == S.KIND_COMPRESSED
+
+
+@pytest.mark.gpu
+def test_compressed_roundtrip_byte_exact(blobs, golden_params):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import compress as CP
+    p = B.gen_params(**golden_params["small"]["kwargs"])
+    cp = S.load_plaintext_auto(blobs["compressed"], p)
+    assert isinstance(cp, CP.CompressedPlaintext) and cp.descriptor.stride == 8 and cp.level == 3
+    own = CP.encode_compressed(np.tile(np.linspace(-0.5, 0.75, 8), p.n // 8), p, stride=8, level=3)
+    assert torch.equal(cp.unique, own.unique) and cp.scale == own.scale
+    assert S.compressed_to_bytes(cp, p) == blobs["compressed"]
+    assert S.compressed_to_bytes(own, p) == blobs["compressed"]
+    assert isinstance(S.load_plaintext_auto(blobs["plaintext"], p), B.Plaintext)
