@@ -274,6 +274,55 @@ int lf_ptmac_rows(const lf_ctx* ctx, uint32_t* out, int nrows, const int32_t* pr
 int lf_mul_compressed(const lf_ctx* ctx, uint32_t* out, const uint32_t* ct, const uint32_t* unique,
                       int nrows, int unique_count, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Limb-sharded keyswitch over k GPUs (reference multidev.py).  Placement as the
+ * reference's partitioner (multidev.py:55-56): main row i on rank i % k, special row j on
+ * rank j % k.  Each rank holds only its rows of the ciphertexts AND of the evaluation keys
+ * (key rows: main_loc(L) ascending, then special_loc: lf_shard_info n_key_rows), and runs the
+ * fused pipeline on them; the InputBroadcast exchange (multidev.py:172-185, 291-412) is two
+ * all-gathers per keyswitch: the (l+1) row-INTT'd digit rows before the ModUp conversion and
+ * the 2 alpha row-INTT'd special rows before ModDown.  Results are bit-identical to
+ * lf_keyswitch / lf_hom_mul / lf_rotate restricted to the rank's rows.
+ *   op 0 keyswitch(x):  x = local rows of x, out = (ks_b, ks_a) local rows (keyswitch, ckks.py:134-140)
+ *   op 1 hom_mul:       x = local a1 rows, x2 = local a2 rows, e0/e1 = local ct1/ct2 blocks (ckks.py:182-194)
+ *   op 2 hom_rotate:    x = local ct.a rows, e0 = local ct block, galois[b] (ckks.py:197-217)
+ * Blocks are (2, n_main, N) (b rows then a rows); strides are in words. */
+typedef struct lf_shard lf_shard;
+typedef struct lf_comm lf_comm;
+typedef struct lf_shard_call {
+  int level, op, batch;                 /* batch <= 64 */
+  const uint32_t* x;
+  const uint32_t* x2;
+  size_t x_bstride;
+  const uint32_t* const* keys;          /* per instance: the rank's key rows (d, 2, n_key_rows, N) */
+  const uint32_t* galois;               /* per instance (op 2), host array */
+  uint32_t* out;
+  size_t out_bstride;
+  const uint32_t* e0;
+  const uint32_t* e1;
+  size_t e_bstride;
+} lf_shard_call;
+int lf_shard_create(const lf_ctx* ctx, int k, int rank, lf_shard** out);
+int lf_shard_destroy(lf_shard* sh);
+int lf_shard_info(const lf_shard* sh, int level, int* n_main, int* n_ext, int* n_key_rows, int* n_special);
+size_t lf_shard_ws_bytes(const lf_shard* sh, int level, int batch);
+/* byte offsets inside the workspace and per-rank byte counts of the two gathers:
+ * {ModUp send, ModUp bytes, ModUp recv, ModDown send, ModDown bytes, ModDown recv};
+ * recv holds the k ranks' send buffers back to back (an all-gather). */
+int lf_shard_gather_layout(const lf_shard* sh, int level, int batch, size_t* out6);
+/* one phase (0: before the ModUp gather, 1: between the gathers, 2: after the ModDown gather),
+ * for callers that perform the all-gathers themselves */
+int lf_shard_ks_phase(const lf_shard* sh, int phase, const lf_shard_call* call, void* workspace, void* stream);
+/* NCCL communicator owned by the library (libnccl.so.2 resolved at run time): rank 0 creates
+ * the 128-byte unique id, the caller broadcasts it, every rank calls lf_comm_create. */
+int lf_comm_unique_id(void* out128);
+int lf_comm_create(int nranks, int rank, const void* id128, lf_comm** out);
+int lf_comm_destroy(lf_comm* comm);
+int lf_shard_attach_comm(lf_shard* sh, lf_comm* comm);
+/* the whole sharded keyswitch on `stream`, both all-gathers through the attached communicator
+ * (ncclAllGather on the same stream: asynchronous, graph-capturable, no host synchronisation) */
+int lf_shard_keyswitch(const lf_shard* sh, const lf_shard_call* call, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,17 @@ def _load():
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     sig = {
+        "lf_shard_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+        "lf_shard_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+        "lf_shard_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 4),
+        "lf_shard_ws_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+        "lf_shard_gather_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+        "lf_shard_ks_phase": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+        "lf_comm_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+        "lf_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+        "lf_shard_attach_comm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_shard_keyswitch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
         "lf_abi_version": (ctypes.c_int, []),
         "lf_last_error": (ctypes.c_char_p, []),
         "lf_set_bconv_engine": (ctypes.c_int, [ctypes.c_int]),

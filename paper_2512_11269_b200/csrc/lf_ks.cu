@@ -41,11 +41,17 @@ LF_DEV void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+struct BcGroupDev;
+LF_DEV int bc_src_row(int row0, int sr, int rstride) { return row0 + (sr & 0xFFFF) + (sr >> 16) * rstride; }
+
 struct BcArgs {
   const u32* src;
   u32* dst;
   size_t src_bs, dst_bs;     // batch strides (words)
   int ngroups, tsplit;
+  // limb-sharded pipeline: source rows gathered from k ranks; src_rows[i] = (rank << 16) | slot
+  // and the row is slot + rank * src_rstride (0: plain row indices)
+  int src_rstride;
   BcGroupDev g[LF_BC_MAXG];
 };
 
@@ -55,15 +61,15 @@ template <int L1, int L2, int MODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
            size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase,
-           int nbatch, int bpc) {
+           int nbatch, int bpc, int pstep) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int GROUPS = (1 << L1) / S::LPCR;
   extern __shared__ __align__(16) u32 sm[];
   const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
   const int row = blockIdx.x / GROUPS, hi0 = (blockIdx.x % GROUPS) * S::LPCR, hi = hi0 + ln;
-  // row r: source row (r / rpp) * src_rs + src_r0 + r % rpp, prime pbase + r % rpp
-  const int pi = pbase + row % rpp;
+  // row r: source row (r / rpp) * src_rs + src_r0 + r % rpp, prime pbase + pstep * (r % rpp)
+  const int pi = pbase + pstep * (row % rpp);
   const PrimeK pk = dv.pk[pi];
   uint2* tws = reinterpret_cast<uint2*>(sm);
   __shared__ unsigned long long twbar;
@@ -269,7 +275,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
-    load_col_step2<L1, L2>(x, src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col, tl);
+    load_col_step2<L1, L2>(x, src + ((size_t)bc_src_row(G.src_row0, G.src_rows[i], A.src_rstride) << logN) + col, tl);
     inv_line<L1>(x, 1u, TwGlobalT<L1>{dv.twiT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
@@ -439,7 +445,7 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
-    load_col_step2<L1, L2>(x, src + ((size_t)(G.src_row0 + G.src_rows[i]) << logN) + col, tl);
+    load_col_step2<L1, L2>(x, src + ((size_t)bc_src_row(G.src_row0, G.src_rows[i], A.src_rstride) << logN) + col, tl);
     inv_line<L1>(x, 1u, TwGlobalT<L1>{dv.twiT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
@@ -569,6 +575,12 @@ struct KsInnerArgs {
   int c_ne;
   const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
   u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
+  // limb-sharded pipeline (null tmap: one device holds every row): CTA row r of this rank's
+  // extended rows is ext position tmap[r] and key row kmap[r]; storage holds n_main_st main
+  // rows then the special rows, ext_st rows per digit in T1
+  const int* tmap;
+  const int* kmap;
+  int n_main_st, ext_st;
 };
 
 #ifndef LF_KSI_MINB
@@ -592,13 +604,17 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   const int groups = (1 << L1) / S::LPCR;
   const size_t b = blockIdx.x % A.nbatch;
   const int bl = blockIdx.x / A.nbatch;
-  const int t = bl / groups;                                 // ext position
+  const int r = bl / groups;                                 // storage row
+  const int t = A.tmap ? A.tmap[r] : r;                      // ext position
   const int hi = (bl % groups) * S::LPCR + ln;
   const int l = A.level;
   const bool is_main = t <= l;
-  const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index == key row
+  const int pi = is_main ? t : A.L + 1 + (t - l - 1);       // prime index
+  const int kr = A.kmap ? A.kmap[r] : pi;                    // key row
   const PrimeK pk = dv.pk[pi];
-  const int ext = l + 1 + A.alpha;
+  const int ext = A.tmap ? A.ext_st : l + 1 + A.alpha;      // T1 rows per digit
+  const int nms = A.tmap ? A.n_main_st : l + 1;             // main rows in storage
+  const int rs = is_main ? r : r - nms;                      // storage index within main / special
   u32* xs = rowpass_xs<L1, L2>(sm) + ln * (pitchR<L2>() + M2);
   u32* perm_buf = xs + pitchR<L2>();
   const AddrR<L2> addr{0};
@@ -622,9 +638,9 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     if (j >= A.beta) return;
     const size_t lo = ((size_t)hk << L2) + (size_t)tl * C::E;
     if (j != own_j || A.pre)
-      prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
-    prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + lo);
-    prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + lo);
+      prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + r) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
+    prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + kr) << logN) + lo);
+    prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + kr) << logN) + lo);
   };
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
@@ -643,7 +659,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     u32 pc[C::E];
     if (A.pre) {
       // finished piece: load the source line, permute inside it (sigma_g) through smem
-      load_row_step2<L2>(pc, A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2), tl);
+      load_row_step2<L2>(pc, A.T1 + b * A.t1_bs + ((size_t)(j * ext + r) << logN) + ((size_t)hs << L2), tl);
       if (GALOIS && !KP) {
         __syncwarp();                  // previous digit's gathers from perm_buf are done
 #pragma unroll
@@ -658,7 +674,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     } else if (j == own_j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
       const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
-      const u32* xr = A.x + b * A.x_bs + ((size_t)t << logN);
+      const u32* xr = A.x + b * A.x_bs + ((size_t)r << logN);
       if (GALOIS) {
         // the source line, coalesced; sigma_g through the line's slot buffer (GMODE 1)
         load_row_step2<L2>(pc, xr + ((size_t)hs << L2), tl);
@@ -676,7 +692,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
           }
         }
       } else {
-        const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)t << logN);
+        const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)r << logN);
         load_row_step2<L2>(pc, xr + ((size_t)hi << L2), tl);
         if (XMODE == 1) {
           u32 w[C::E];
@@ -688,7 +704,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
         for (int e = 0; e < C::E; ++e) pc[e] = mul_shoup_lazy(pc[e], s, sp, pk.q);
       }
     } else {
-      const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + t) << logN) + ((size_t)hs << L2);
+      const u32* tr = A.T1 + b * A.t1_bs + ((size_t)(j * ext + r) << logN) + ((size_t)hs << L2);
       load_row_step2<L2>(pc, tr, tl);
       fwd_line<L2, BIN>(pc, (1u << L1) + hs, TwTree<L2>{tws, (1u << L1) + hi0s, S::LPCR}, pk.q, xs,
                         tl, addr, SyncWarp{});
@@ -712,10 +728,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       // key rows are loaded only now (L1-prefetched one digit ahead): keeping them live across
       // the row NTT would push the kernel past 128 registers and spill the twiddle addresses
       u32 kv[C::E];
-      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + ((size_t)hk << L2), tl);
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 0) * A.R + kr) << logN) + ((size_t)hk << L2), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) accb[e] += (u64)pc[e] * kv[e];
-      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + ((size_t)hk << L2), tl);
+      load_row_step2<L2>(kv, keyb + (((size_t)(j * 2 + 1) * A.R + kr) << logN) + ((size_t)hk << L2), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) acca[e] += (u64)pc[e] * kv[e];
     }
@@ -761,12 +777,12 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
     store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(ext + t) << logN) + ((size_t)hi << L2), tl);
   } else if (is_main && t <= l - A.fuse_nd) {
-    store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)t << logN) + ((size_t)hi << L2), tl);
-    store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(rb, A.acc + b * A.acc_bs + ((size_t)rs << logN) + ((size_t)hi << L2), tl);
+    store_row_step2<L2>(ra, A.acc + b * A.acc_bs + ((size_t)(nms + rs) << logN) + ((size_t)hi << L2), tl);
   } else {
     // special row, or (fused rescale) one of the top main rows: T2 holds the rows the division
     // by P q_l [q_{l-1}] converts, in coefficient form after the row pass of the INTT
-    const int s = is_main ? A.alpha + (t - (l + 1 - A.fuse_nd)) : t - l - 1;
+    const int s = is_main ? A.alpha + (t - (l + 1 - A.fuse_nd)) : rs;
     if (XMODE == 1 && is_main) {
       // + P * (d0, d1) (ckks.py:189-193: d0 = b1 b2, d1 = b1 a2 + a1 b2) before the division
       const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
@@ -959,6 +975,7 @@ struct ModDownArgs {
   int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
   int nbatch, bpc;     // instances; instances per CTA (sharing the staged twiddles)
   u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
+  const int* tmap;     // limb-sharded: storage row r is main prime tmap[r] (null: r)
 };
 
 template <int L1, int L2, int EPI>
@@ -971,15 +988,16 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
   extern __shared__ u32 sm[];
   const int tl = threadIdx.x % C::T, ln = threadIdx.x / C::T;
   const int groups = (1 << L1) / S::LPCR;
-  const int t = blockIdx.x / groups;
+  const int t = blockIdx.x / groups;                   // storage row
+  const int pi = A.tmap ? A.tmap[t] : t;               // main prime index
   const int hi = (blockIdx.x % groups) * S::LPCR + ln;
-  const PrimeK pk = dv.pk[t];
-  const u32 sc = A.scal[t * A.sstride], scp = A.scal[t * A.sstride + 1];
+  const PrimeK pk = dv.pk[pi];
+  const u32 sc = A.scal[pi * A.sstride], scp = A.scal[pi * A.sstride + 1];
   uint2* tws = reinterpret_cast<uint2*>(sm);
   const u32 R0 = (1u << L1) + (blockIdx.x % groups) * S::LPCR;
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
-  tw_bulk_begin<L2>(tws, dv.twfT + ((size_t)t << logN), R0, S::LPCR, &twbar);
+  tw_bulk_begin<L2>(tws, dv.twfT + ((size_t)pi << logN), R0, S::LPCR, &twbar);
   lf_pdl_wait();
   const TwTree<L2> tw{tws, R0, S::LPCR};
   u32* xs = rowpass_xs<L1, L2>(sm);
@@ -1017,7 +1035,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
       u32 b1[C::E], b2[C::E], o1[C::E], o2[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo0, tl);
       load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo0, tl);
-      const u32 ds = A.dscal ? A.dscal[2 * t] : 0u, dsp = A.dscal ? A.dscal[2 * t + 1] : 0u;
+      const u32 ds = A.dscal ? A.dscal[2 * pi] : 0u, dsp = A.dscal ? A.dscal[2 * pi + 1] : 0u;
       if (p == 0) {
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
@@ -1282,9 +1300,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     const int bpc_in = nsh >= 2 * LF_BPC ? LF_BPC : 1;      // instances per CTA (shared twiddles)
     dim3 grid(l1 * groups, 1, (nsh + bpc_in - 1) / bpc_in);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1)); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -1418,7 +1436,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt, batch, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt, batch, 1, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1462,7 +1480,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
   u32* T3 = T2 + 2 * (size_t)alpha * N;
   {
     dim3 grid(2 * alpha * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1507,7 +1525,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1836,6 +1854,317 @@ int lf_ks_decompose(const lf_ctx* ctx, int level, const uint32_t* x, uint32_t* p
   LF_DISPATCH_LOGN(ctx->logN, LF_DC)
 #undef LF_DC
   return 0;
+}
+
+}  // extern "C"
+
+// =======================================================================================
+// Limb-sharded keyswitch (reference multidev.py:55-56 placement, InputBroadcast
+// pattern multidev.py:172-185, 291-412).  The five fused kernels run on this rank's rows only;
+// the two cross-limb stages read all-gathered buffers:
+//   phase 0  K_A  row INTT of the local main rows of x            -> T0s (m_slots rows)
+//   gather   T0s of every rank                                    -> T0g
+//   phase 1  K_BC ModUp: every digit's sources from T0g, targets = local extended rows;
+//            K_C  row NTT + key inner product with the LOCAL key rows; local special rows'
+//            row INTT                                             -> acc, T2s (2 s_slots rows)
+//   gather   T2s of every rank                                    -> T2g
+//   phase 2  K_BC ModDown from T2g onto the local main rows; K_E (acc - conv) P^-1 + epilogue
+// Modular sums are associative and the gathers move exact residues, so every output residue
+// equals the single-device pipeline's.
+#include <dlfcn.h>
+#include <nccl.h>
+
+struct lf_comm {
+  ncclComm_t comm;
+  int nranks, rank;
+};
+
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*err)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+// NCCL is resolved at run time from the libnccl already loaded by the process (torch's), so
+// the library never carries a second NCCL.
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_id = (decltype(a.get_id))dlsym(h, "ncclGetUniqueId");
+    a.init_rank = (decltype(a.init_rank))dlsym(h, "ncclCommInitRank");
+    a.all_gather = (decltype(a.all_gather))dlsym(h, "ncclAllGather");
+    a.destroy = (decltype(a.destroy))dlsym(h, "ncclCommDestroy");
+    a.err = (decltype(a.err))dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_id && a.init_rank && a.all_gather && a.destroy && a.err;
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+struct ShardWs {
+  u32 *T0s, *T0g, *T1, *acc, *T2s, *T2g, *T3;
+  size_t t0_rows, t2_rows;       // rows each rank sends per gather (whole batch)
+};
+
+static ShardWs shard_carve(const LfCtx* ctx, const LfShardPlan* P, int level, int batch, void* ws) {
+  const ShardLevel& S = P->lv[level];
+  const size_t N = ctx->N, B = batch;
+  ShardWs w;
+  u32* p = (u32*)ws;
+  w.t0_rows = B * S.m_slots;
+  w.t2_rows = B * 2 * P->s_slots;
+  w.T0s = p; p += w.t0_rows * N;
+  w.T0g = p; p += P->k * w.t0_rows * N;
+  w.T1 = p;  p += B * S.beta * S.ext * N;
+  w.acc = p; p += B * 2 * S.n_main * N;
+  w.T2s = p; p += w.t2_rows * N;
+  w.T2g = p; p += P->k * w.t2_rows * N;
+  w.T3 = p;  p += B * 2 * S.n_main * N;
+  return w;
+}
+static size_t shard_ws_words(const LfCtx* ctx, const LfShardPlan* P, int level, int batch) {
+  ShardWs w = shard_carve(ctx, P, level, batch, nullptr);
+  return (size_t)(w.T3 - (u32*)nullptr) + (size_t)batch * 2 * P->lv[level].n_main * ctx->N;
+}
+
+template <int L1, int L2>
+static int shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const lf_shard_call* c, void* ws,
+                       cudaStream_t s) {
+  using S_ = NttShape<L1, L2>;
+  const LfKsPlan* K = ctx->ks;
+  const int level = c->level, B = c->batch;
+  const ShardLevel& S = P->lv[level];
+  const ShardWs w = shard_carve(ctx, P, level, B, ws);
+  const size_t N = ctx->N;
+  const LfDev dv = ctx->dev();
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
+  const int groups = (1 << L1) / S_::LPCR;
+  const int nm = S.n_main;
+  if (phase == 0) {
+    if (nm == 0) return 0;
+    const int bpc = B >= 2 * LF_BPC ? LF_BPC : 1;
+    dim3 grid(nm * groups, 1, (B + bpc - 1) / bpc);
+    const size_t tbs = (size_t)S.m_slots * N;
+    if (c->op == OP_MUL) { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, grid, dim3(S_::TRR), smR, s, 1, c->x, c->x2, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k)); }
+    else { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, grid, dim3(S_::TRR), smR, s, 1, c->x, (const u32*)nullptr, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k)); }
+    LF_CHECK_LAUNCH();
+    return 0;
+  }
+  if (phase == 1) {
+    {   // K_BC ModUp
+      BcArgs A{};
+      A.src = w.T0g; A.dst = w.T1; A.src_bs = (size_t)S.m_slots * N; A.dst_bs = (size_t)S.beta * S.ext * N;
+      A.src_rstride = (int)w.t0_rows;
+      int kmax = 0, mmax = 0, ng = 0;
+      for (int j = 0; j < S.beta; ++j) {
+        if (!S.up_m[j]) continue;
+        A.g[ng] = S.up[j];
+        kmax = S.up[j].B.k > kmax ? S.up[j].B.k : kmax;
+        mmax = S.up[j].B.m > mmax ? S.up[j].B.m : mmax;
+        ++ng;
+      }
+      A.ngroups = ng;
+      if (ng) {
+        A.tsplit = bc_tsplit(ng, B, (1 << L2) / 8, mmax, env_int("LF_TSPLIT_UP", 96));
+        if (int e = launch_bc_auto<L1, L2>(ctx, A, B, kmax, s)) return e;
+      }
+    }
+    {   // K_C
+      KsInnerArgs A{};
+      A.T1 = w.T1; A.x = c->x; A.x2 = c->x2 ? c->x2 : c->x; A.acc = w.acc; A.T2 = w.T2s;
+      A.t1_bs = (size_t)S.beta * S.ext * N; A.x_bs = c->x_bstride; A.acc_bs = (size_t)2 * nm * N;
+      A.t2_bs = (size_t)2 * P->s_slots * N;
+      A.rowk = K->rowk; A.level = level; A.d = K->d; A.beta = S.beta; A.L = K->L; A.alpha = K->n_special;
+      A.R = P->n_key_rows; A.nbatch = B; A.pre = 0; A.ext_out = 0; A.fuse_nd = 0; A.t2_rows = P->s_slots;
+      A.pmod = K->pmod;
+      A.tmap = S.tmap; A.kmap = S.kmap; A.n_main_st = nm; A.ext_st = S.ext;
+      for (int b = 0; b < B; ++b) { A.keyp[b] = c->keys[b]; A.gs[b] = c->galois ? c->galois[b] : 1u; }
+      const size_t smC = rowpass_smem_bytes<L1, L2>(LineCfg<L2>::M);
+      dim3 grid(S.ext * groups * B);
+      if (S.ext) {
+        if (c->op == OP_ROT) { lf_smem_optin(k_ks_inner<L1, L2, 1, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 1, 0>, grid, dim3(S_::TRR), smC, s, 1, A, dv)); }
+        else if (c->op == OP_MUL) { lf_smem_optin(k_ks_inner<L1, L2, 0, 1>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 0, 1>, grid, dim3(S_::TRR), smC, s, 1, A, dv)); }
+        else { lf_smem_optin(k_ks_inner<L1, L2, 0, 0>, smC); LF_LAUNCH_CHECK(lf_launch(k_ks_inner<L1, L2, 0, 0>, grid, dim3(S_::TRR), smC, s, 1, A, dv)); }
+        LF_CHECK_LAUNCH();
+      }
+    }
+    return 0;
+  }
+  if (nm == 0) return 0;
+  {   // K_BC ModDown
+    BcArgs A{};
+    A.src = w.T2g; A.dst = w.T3; A.src_bs = (size_t)2 * P->s_slots * N; A.dst_bs = (size_t)2 * nm * N;
+    A.src_rstride = (int)w.t2_rows;
+    A.ngroups = 2;
+    for (int p = 0; p < 2; ++p) {
+      A.g[p] = P->down[p];
+      A.g[p].B.m = nm;                     // prefix of the level-L local table
+      A.g[p].dst_row0 = p * nm;
+    }
+    A.tsplit = bc_tsplit(2, B, (1 << L2) / 8, nm, env_int("LF_TSPLIT_DOWN", 96));
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, B, K->n_special, s)) return e;
+  }
+  {   // K_E
+    ModDownArgs A{};
+    A.T3 = w.T3; A.acc = w.acc; A.out = c->out; A.e0 = c->e0; A.e1 = c->e1;
+    A.t3_bs = (size_t)2 * nm * N; A.acc_bs = A.t3_bs; A.out_bs = c->out_bstride; A.e_bs = c->e_bstride;
+    A.scal = K->rowk + 2; A.sstride = 4; A.nt = nm; A.nacc = nm; A.ne = nm;
+    A.tmap = S.tmap;
+    for (int b = 0; b < B; ++b) A.gs[b] = c->galois ? c->galois[b] : 1u;
+    A.nbatch = B;
+    A.bpc = B >= 2 * LF_BPC ? LF_BPC : 1;
+    dim3 grid(nm * groups, 1, (B + A.bpc - 1) / A.bpc);
+    if (c->op == OP_MUL) { lf_smem_optin(k_moddown_out<L1, L2, EPI_MUL>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_MUL>, grid, dim3(S_::TRR), smR, s, 1, A, dv)); }
+    else if (c->op == OP_ROT) { lf_smem_optin(k_moddown_out<L1, L2, EPI_ROT>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_ROT>, grid, dim3(S_::TRR), smR, s, 1, A, dv)); }
+    else { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, grid, dim3(S_::TRR), smR, s, 1, A, dv)); }
+    LF_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+static int run_shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const lf_shard_call* c, void* ws,
+                           cudaStream_t s) {
+#define LF_SH(A, B_) { if (int e = shard_phase<A, B_>(ctx, P, phase, c, ws, s)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_SH)
+#undef LF_SH
+  return 0;
+}
+
+extern "C" {
+
+struct lf_shard {
+  const LfCtx* ctx;
+  LfShardPlan* plan;
+};
+
+int lf_shard_create(const lf_ctx* ctx, int k, int rank, lf_shard** out) {
+  if (!ctx || !out) { lf_set_error("lf_shard_create: null argument"); return 1; }
+  LfShardPlan* P = nullptr;
+  if (int e = lf_build_shard_plan(ctx, k, rank, &P)) return e;
+  *out = new lf_shard{ctx, P};
+  return 0;
+}
+
+int lf_shard_destroy(lf_shard* sh) {
+  if (!sh) return 0;
+  lf_free_shard_plan(sh->plan);
+  delete sh;
+  return 0;
+}
+
+int lf_shard_info(const lf_shard* sh, int level, int* n_main, int* n_ext, int* n_key_rows, int* n_special) {
+  if (!sh || level < 0 || level > sh->plan->L) { lf_set_error("lf_shard_info: bad shard or level"); return 1; }
+  const ShardLevel& S = sh->plan->lv[level];
+  if (n_main) *n_main = S.n_main;
+  if (n_ext) *n_ext = S.ext;
+  if (n_key_rows) *n_key_rows = sh->plan->n_key_rows;
+  if (n_special) *n_special = sh->plan->n_sp;
+  return 0;
+}
+
+size_t lf_shard_ws_bytes(const lf_shard* sh, int level, int batch) {
+  if (!sh || level < 0 || level > sh->plan->L || batch < 1) return 0;
+  return shard_ws_words(sh->ctx, sh->plan, level, batch) * 4;
+}
+
+int lf_shard_gather_layout(const lf_shard* sh, int level, int batch, size_t* out6) {
+  if (!sh || !out6 || level < 0 || level > sh->plan->L || batch < 1) { lf_set_error("lf_shard_gather_layout: bad argument"); return 1; }
+  const ShardWs w = shard_carve(sh->ctx, sh->plan, level, batch, nullptr);
+  const size_t rb = (size_t)sh->ctx->N * 4;
+  out6[0] = (size_t)((char*)w.T0s - (char*)nullptr); out6[1] = w.t0_rows * rb; out6[2] = (size_t)((char*)w.T0g - (char*)nullptr);
+  out6[3] = (size_t)((char*)w.T2s - (char*)nullptr); out6[4] = w.t2_rows * rb; out6[5] = (size_t)((char*)w.T2g - (char*)nullptr);
+  return 0;
+}
+
+static int shard_check(const lf_shard* sh, const lf_shard_call* c, void* ws) {
+  if (!sh || !c || !ws) { lf_set_error("sharded keyswitch: null argument"); return 1; }
+  if (c->level < 0 || c->level > sh->plan->L) { lf_set_error("sharded keyswitch: level %d", c->level); return 2; }
+  if (c->batch < 1 || c->batch > LF_MAXB) { lf_set_error("sharded keyswitch: batch %d outside [1, %d]", c->batch, LF_MAXB); return 2; }
+  if (c->op != OP_KS && c->op != OP_MUL && c->op != OP_ROT) { lf_set_error("sharded keyswitch: op %d", c->op); return 2; }
+  if (!c->keys || (sh->plan->lv[c->level].n_main && (!c->x || !c->out))) { lf_set_error("sharded keyswitch: null argument"); return 1; }
+  if ((c->op == OP_MUL && (!c->x2 || !c->e0 || !c->e1)) || (c->op == OP_ROT && (!c->e0 || !c->galois))) {
+    lf_set_error("sharded keyswitch: op %d needs its epilogue operands", c->op);
+    return 1;
+  }
+  return 0;
+}
+
+int lf_shard_ks_phase(const lf_shard* sh, int phase, const lf_shard_call* call, void* ws, void* stream) {
+  if (int e = shard_check(sh, call, ws)) return e;
+  if (phase < 0 || phase > 2) { lf_set_error("lf_shard_ks_phase: phase %d", phase); return 2; }
+  return run_shard_phase(sh->ctx, sh->plan, phase, call, ws, (cudaStream_t)stream);
+}
+
+int lf_comm_unique_id(void* out128) {
+  const NcclApi& a = nccl();
+  if (!a.ok) { lf_set_error("NCCL not available (libnccl.so.2)"); return 3; }
+  ncclUniqueId id;
+  ncclResult_t r = a.get_id(&id);
+  if (r != ncclSuccess) { lf_set_error("ncclGetUniqueId: %s", a.err(r)); return 3; }
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int lf_comm_create(int nranks, int rank, const void* id128, lf_comm** out) {
+  const NcclApi& a = nccl();
+  if (!a.ok) { lf_set_error("NCCL not available (libnccl.so.2)"); return 3; }
+  if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) { lf_set_error("lf_comm_create: bad argument"); return 1; }
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  lf_comm* c = new lf_comm{nullptr, nranks, rank};
+  ncclResult_t r = a.init_rank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) { delete c; lf_set_error("ncclCommInitRank: %s", a.err(r)); return 3; }
+  *out = c;
+  return 0;
+}
+
+int lf_comm_destroy(lf_comm* c) {
+  if (!c) return 0;
+  if (c->comm) nccl().destroy(c->comm);
+  delete c;
+  return 0;
+}
+
+int lf_shard_attach_comm(lf_shard* sh, lf_comm* comm) {
+  if (!sh) { lf_set_error("lf_shard_attach_comm: null shard"); return 1; }
+  if (comm && (comm->nranks != sh->plan->k || comm->rank != sh->plan->rank)) {
+    lf_set_error("lf_shard_attach_comm: communicator rank %d/%d, shard %d/%d", comm->rank, comm->nranks,
+                 sh->plan->rank, sh->plan->k);
+    return 2;
+  }
+  sh->plan->comm = comm;
+  return 0;
+}
+
+int lf_shard_keyswitch(const lf_shard* sh, const lf_shard_call* call, void* ws, void* stream) {
+  if (int e = shard_check(sh, call, ws)) return e;
+  lf_comm* cm = (lf_comm*)sh->plan->comm;
+  if (!cm && sh->plan->k > 1) { lf_set_error("lf_shard_keyswitch: no communicator attached (lf_shard_attach_comm)"); return 2; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const ShardWs w = shard_carve(sh->ctx, sh->plan, call->level, call->batch, ws);
+  const size_t rb = (size_t)sh->ctx->N * 4;
+  if (int e = run_shard_phase(sh->ctx, sh->plan, 0, call, ws, s)) return e;
+  if (cm) {
+    ncclResult_t r = nccl().all_gather(w.T0s, w.T0g, w.t0_rows * rb, ncclUint8, cm->comm, s);
+    if (r != ncclSuccess) { lf_set_error("ncclAllGather (ModUp): %s", nccl().err(r)); return 3; }
+  } else if (cudaMemcpyAsync(w.T0g, w.T0s, w.t0_rows * rb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    lf_set_error("sharded keyswitch: copy failed"); return 3;
+  }
+  if (int e = run_shard_phase(sh->ctx, sh->plan, 1, call, ws, s)) return e;
+  if (cm) {
+    ncclResult_t r = nccl().all_gather(w.T2s, w.T2g, w.t2_rows * rb, ncclUint8, cm->comm, s);
+    if (r != ncclSuccess) { lf_set_error("ncclAllGather (ModDown): %s", nccl().err(r)); return 3; }
+  } else if (cudaMemcpyAsync(w.T2g, w.T2s, w.t2_rows * rb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    lf_set_error("sharded keyswitch: copy failed"); return 3;
+  }
+  return run_shard_phase(sh->ctx, sh->plan, 2, call, ws, s);
 }
 
 }  // extern "C"

@@ -350,6 +350,130 @@ int lf_build_ks_plan(LfCtx* ctx, int n_main, int d) {
   return 0;
 }
 
+int lf_build_shard_plan(const LfCtx* ctx, int k, int rank, LfShardPlan** out) {
+  const LfKsPlan* K = ctx->ks;
+  if (!K) { lf_set_error("shard plan: keyswitch plans not built"); return 2; }
+  if (k < 1 || k > 64 || rank < 0 || rank >= k) { lf_set_error("shard plan: rank %d of %d", rank, k); return 2; }
+  const int n_main = K->n_main, n_sp = K->n_special, d = K->d, L = K->L;
+  std::vector<u32> primes(ctx->nprimes), ninv(ctx->nprimes);
+  for (int i = 0; i < ctx->nprimes; ++i) { primes[i] = ctx->h_pk[i].q; ninv[i] = ctx->h_pk[i].ninv; }
+  auto dec_scalar = [&](int j, int i) {
+    const u32 q = primes[i];
+    u32 f = 1;
+    for (int t = 0; t <= L; ++t)
+      if (t % d != j) f = mulm(f, primes[t] % q, q);
+    return invm(f, q);
+  };
+  std::vector<int> sp_loc;
+  for (int j = rank; j < n_sp; j += k) sp_loc.push_back(j);
+  const int s_slots = (n_sp + k - 1) / k;
+  int n_main_L = 0;
+  for (int i = rank; i <= L; i += k) ++n_main_L;
+  Blob blob;
+  blob.w.push_back(0);                      // offset 0 means "none" for the w8 tables
+  struct LvRec {
+    int n_main, ext, beta, m_slots;
+    size_t tmap, kmap;
+    TabRec up[LF_MAXD];
+    size_t src_off[LF_MAXD], dst_off[LF_MAXD];
+    int up_m[LF_MAXD];
+  };
+  std::vector<LvRec> lvr(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    LvRec& R = lvr[l];
+    std::vector<int> pos, krow;               // local rows: main (ascending), then special
+    for (int i = rank; i <= l; i += k) { pos.push_back(i); krow.push_back(i / k); }
+    R.n_main = (int)pos.size();
+    for (int j : sp_loc) { pos.push_back(l + 1 + j); krow.push_back(n_main_L + j / k); }
+    R.ext = (int)pos.size();
+    R.beta = d < l + 1 ? d : l + 1;
+    R.m_slots = (l + 1 + k - 1) / k;
+    R.tmap = blob.push(std::vector<u32>(pos.begin(), pos.end()));
+    R.kmap = blob.push(std::vector<u32>(krow.begin(), krow.end()));
+    for (int j = 0; j < R.beta; ++j) {
+      std::vector<int> src, tgt;
+      std::vector<u32> mult, srows, drows;
+      for (int i = j; i <= l; i += d) {
+        src.push_back(i);
+        mult.push_back(mulm(ninv[i], dec_scalar(j, i), primes[i]));
+        srows.push_back(((u32)(i % k) << 16) | (u32)(i / k));
+      }
+      for (int r = 0; r < R.ext; ++r) {
+        const int t = pos[r];
+        if (t <= l && t % d == j) continue;
+        tgt.push_back(t <= l ? t : n_main + (t - l - 1));
+        drows.push_back((u32)(j * R.ext + r));
+      }
+      R.up_m[j] = (int)tgt.size();
+      if (tgt.empty()) { tgt.push_back(0); drows.push_back(0); }     // idle group: never launched
+      R.up[j] = build_table(blob, primes, src, tgt, mult);
+      R.src_off[j] = blob.push(srows);
+      R.dst_off[j] = blob.push(drows);
+    }
+  }
+  // ModDown: all specials -> local main rows at L (a prefix serves every level)
+  std::vector<int> sp_src, main_loc_L;
+  std::vector<u32> sp_mult, dsrc[2], iota;
+  for (int j = 0; j < n_sp; ++j) {
+    sp_src.push_back(n_main + j);
+    sp_mult.push_back(ninv[n_main + j]);
+    for (int p = 0; p < 2; ++p) dsrc[p].push_back(((u32)(j % k) << 16) | (u32)(p * s_slots + j / k));
+  }
+  for (int i = rank; i <= L; i += k) main_loc_L.push_back(i);
+  if (main_loc_L.empty()) main_loc_L.push_back(0);      // a rank without main rows (k > L+1)
+  for (size_t i = 0; i < main_loc_L.size(); ++i) iota.push_back((u32)i);
+  const TabRec down = build_table(blob, primes, sp_src, main_loc_L, sp_mult);
+  const size_t off_dsrc0 = blob.push(dsrc[0]), off_dsrc1 = blob.push(dsrc[1]), off_iota = blob.push(iota);
+
+  void* dmem = nullptr;
+  if (cudaMalloc(&dmem, blob.w.size() * 4) != cudaSuccess ||
+      cudaMemcpy(dmem, blob.w.data(), blob.w.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    lf_set_error("shard plan: device allocation failed");
+    return 3;
+  }
+  const u32* base = (const u32*)dmem;
+  auto view = [&](const TabRec& r) {
+    BconvDev v = lf_bconv_view(base + r.off, r.k, r.m, r.W);
+    if (r.w8off) { v.w8 = (const unsigned char*)(base + r.w8off); v.kb = r.kb; }
+    return v;
+  };
+  LfShardPlan* P = new LfShardPlan();
+  P->k = k; P->rank = rank; P->L = L; P->alpha = n_sp; P->d = d;
+  P->n_sp = (int)sp_loc.size(); P->s_slots = s_slots; P->n_key_rows = n_main_L + (int)sp_loc.size();
+  P->dmem = dmem; P->comm = nullptr;
+  P->lv.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    ShardLevel& S = P->lv[l];
+    const LvRec& R = lvr[l];
+    S.n_main = R.n_main; S.ext = R.ext; S.beta = R.beta; S.m_slots = R.m_slots;
+    S.tmap = (const int*)(base + R.tmap);
+    S.kmap = (const int*)(base + R.kmap);
+    for (int j = 0; j < R.beta; ++j) {
+      S.up_m[j] = R.up_m[j];
+      S.up[j].B = view(R.up[j]);
+      S.up[j].src_rows = (const int*)(base + R.src_off[j]);
+      S.up[j].dst_rows = (const int*)(base + R.dst_off[j]);
+      S.up[j].src_row0 = 0;
+      S.up[j].dst_row0 = 0;
+    }
+  }
+  for (int p = 0; p < 2; ++p) {
+    P->down[p].B = view(down);
+    P->down[p].src_rows = (const int*)(base + (p ? off_dsrc1 : off_dsrc0));
+    P->down[p].dst_rows = (const int*)(base + off_iota);
+    P->down[p].src_row0 = 0;
+    P->down[p].dst_row0 = 0;          // set per call: p * n_main(level)
+  }
+  *out = P;
+  return 0;
+}
+
+void lf_free_shard_plan(LfShardPlan* p) {
+  if (!p) return;
+  cudaFree(p->dmem);
+  delete p;
+}
+
 void lf_free_ks_plan(LfKsPlan* p) {
   if (!p) return;
   cudaFree(p->dmem);

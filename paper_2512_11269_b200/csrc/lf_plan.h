@@ -42,3 +42,27 @@ struct LfKsPlan {
 
 int lf_build_ks_plan(struct LfCtx* ctx, int n_main, int d);
 void lf_free_ks_plan(LfKsPlan* p);
+
+// Limb-sharded keyswitch plan of ONE rank out of k (reference multidev.py:55-56 placement:
+// main row i on rank i % k, special j on rank j % k).  Local rows are stored main-first in
+// ascending prime order; cross-rank sources come from the all-gathered buffers, whose rows
+// are addressed as (rank << 16) | slot (BcArgs::src_rstride).
+struct ShardLevel {
+  int n_main, ext, beta;         // local main rows at this level, local extended rows, digits
+  int m_slots;                   // T0 rows each rank contributes to the ModUp all-gather
+  int up_m[LF_MAXD];             // real targets of digit group j on this rank (0: group idle)
+  const int* tmap;               // [ext] extended-basis position of local row r
+  const int* kmap;               // [ext] row of the rank's local key (main_loc(L) ++ special_loc)
+  BcGroupDev up[LF_MAXD];        // digit j: all sources G_j (gathered) -> local ext rows not in G_j
+};
+struct LfShardPlan {
+  int k, rank, L, alpha, d;
+  int n_sp, s_slots;             // local special rows; special rows each rank contributes (per poly)
+  int n_key_rows;                // rows of the rank's local key: |main_loc(L)| + n_sp
+  std::vector<ShardLevel> lv;
+  BcGroupDev down[2];            // ModDown of poly p: all alpha specials (gathered) -> local main rows
+  void* dmem;
+  void* comm;                    // lf_comm* (NCCL) or null (the host performs the gathers)
+};
+int lf_build_shard_plan(const struct LfCtx* ctx, int k, int rank, LfShardPlan** out);
+void lf_free_shard_plan(LfShardPlan* p);

@@ -278,3 +278,25 @@ def load_plaintext_auto(data, params):
     if detect_kind(data) == KIND_COMPRESSED:
         return compressed_from_bytes(data, params)
     return plaintext_from_bytes(data, params)
+
+
+def evalkey_shard_from_bytes(data, params, k: int, rank: int):
+    """This rank's rows of an LFHE evaluation key, uploaded straight from the blob: only the
+    rows the limb-sharded pipeline reads on `rank` of `k` (main row i on rank i % k, special j
+    on rank j % k, multidev.py:55-56) cross PCIe; returns (purpose, (d, 2, n_key_rows, N))."""
+    from .poly import extended_ids
+    kind, N, primes, _, _, _, off = parse_header(data)
+    if kind != KIND_EVALKEY:
+        raise ValueError(f"LFHE kind {kind} is not an evaluation key")
+    _check_blob(params, N, primes, extended_ids(params, params.max_level), "evaluation key")
+    tag, rot, ndig = struct.unpack_from("<BIH", data, off)
+    off += struct.calcsize("<BIH")
+    if ndig != params.ks.d:
+        raise ValueError(f"LFHE evaluation key: {ndig} digits but the parameters use d={params.ks.d}")
+    L, alpha = params.max_level, params.num_special
+    local = list(range(rank, L + 1, k)) + [L + 1 + j for j in range(rank, alpha, k)]
+    rows, _ = rows_view(data, off, ndig * 2 * len(primes), N)
+    rows = rows.reshape(ndig, 2, len(primes), N)[:, :, local]
+    _check_residues(np.ascontiguousarray(rows).reshape(-1, N), [primes[i] for i in local], "evaluation key")
+    dev = _upload_rows(np.ascontiguousarray(rows).reshape(-1, N)).view(ndig, 2, len(local), N)
+    return ("relin" if tag == 0 else ("rot", rot)), dev

@@ -305,3 +305,240 @@ def gpu_sharded_keyswitch(params, level: int, x_loc, evk, comm=None, galois=None
 
     ks = ShardedKeyswitch(ops, comm, lay, dec_scalars(params, level), pinv_scalars(params, level))
     return ks.keyswitch(x_loc, key_rows, galois)
+
+
+# ---------------------------------------------------------------------------------------
+# The fused limb-sharded pipeline (csrc/lf_ks.cu, lf_shard_*): the five keyswitch kernels on
+# this rank's rows, the two InputBroadcast all-gathers as ncclAllGather on the launch stream.
+# ---------------------------------------------------------------------------------------
+
+import ctypes as _ct
+
+OP_KS, OP_MUL, OP_ROT = 0, 1, 2
+
+
+class _ShardCall(_ct.Structure):
+    """lf_shard_call (include/lf_b200.h)."""
+    _fields_ = [("level", _ct.c_int), ("op", _ct.c_int), ("batch", _ct.c_int),
+                ("x", _ct.c_void_p), ("x2", _ct.c_void_p), ("x_bstride", _ct.c_size_t),
+                ("keys", _ct.c_void_p), ("galois", _ct.c_void_p),
+                ("out", _ct.c_void_p), ("out_bstride", _ct.c_size_t),
+                ("e0", _ct.c_void_p), ("e1", _ct.c_void_p), ("e_bstride", _ct.c_size_t)]
+
+
+class NcclComm:
+    """An NCCL communicator owned by libcerium_b200 (lf_comm_create).  The 128-byte unique id
+    is created on rank 0 and broadcast over the caller's torch.distributed group."""
+
+    def __init__(self, k: int, rank: int, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import _native
+        lib = _native.lib()
+        uid = (_ct.c_uint8 * 128)()
+        if rank == 0:
+            _native.check(lib.lf_comm_unique_id(_ct.cast(uid, _ct.c_void_p)), "lf_comm_unique_id")
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+        uid = (_ct.c_uint8 * 128)(*t.cpu().tolist())
+        h = _ct.c_void_p()
+        _native.check(lib.lf_comm_create(k, rank, _ct.cast(uid, _ct.c_void_p), _ct.byref(h)), "lf_comm_create")
+        self.handle, self.k, self.rank = h, k, rank
+
+    def __del__(self):
+        try:
+            from . import _native
+            if self.handle:
+                _native.lib().lf_comm_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class ShardEngine:
+    """One rank's share of the limb-sharded keyswitch, hom_mul and hom_rotate (this rank's main
+    rows of every ciphertext, its rows of every evaluation key).  With a communicator the calls
+    run end to end on the device stream (lf_shard_keyswitch); without one, `phase()` exposes
+    the three phases for callers that move the gathered rows themselves (`emulate`)."""
+
+    def __init__(self, params, k: int, rank: int, comm=None):
+        from . import _native
+        from .context import get_context
+        self.params, self.k, self.rank = params, k, rank
+        self.ctx = get_context(params)
+        self.lib = _native.lib()
+        h = _ct.c_void_p()
+        _native.check(self.lib.lf_shard_create(self.ctx.handle, k, rank, _ct.byref(h)), "lf_shard_create")
+        self.handle = h
+        # comm: NcclComm (the library's own ncclAllGather on the launch stream), a
+        # torch.distributed group or "torch" (the default group: all_gather_into_tensor on
+        # workspace views; gloo stages through the host), or None for k = 1
+        self.comm = comm
+        if isinstance(comm, NcclComm):
+            _native.check(self.lib.lf_shard_attach_comm(h, comm.handle), "lf_shard_attach_comm")
+        self._ws = {}
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.lf_shard_destroy(self.handle)
+        except Exception:
+            pass
+
+    # layout ---------------------------------------------------------------------------
+    def info(self, level: int):
+        v = [_ct.c_int() for _ in range(4)]
+        from . import _native
+        _native.check(self.lib.lf_shard_info(self.handle, level, *[_ct.byref(x) for x in v]), "lf_shard_info")
+        return dict(n_main=v[0].value, n_ext=v[1].value, n_key_rows=v[2].value, n_special=v[3].value)
+
+    def main_rows(self, level: int) -> list:
+        """Main prime indices this rank holds at `level` (multidev.py:55-56)."""
+        return list(range(self.rank, level + 1, self.k))
+
+    def key_rows(self) -> list:
+        """Rows of the full-level extended basis this rank keeps of every evaluation key:
+        main_loc(L) ascending, then its special rows (prime index L+1+j)."""
+        L, alpha = self.params.max_level, self.params.num_special
+        return self.main_rows(L) + [L + 1 + j for j in range(self.rank, alpha, self.k)]
+
+    def shard_key(self, evk):
+        """This rank's rows of a full evaluation key ((d, 2, L+1+alpha, N) -> (d, 2, n_key_rows, N))."""
+        import torch
+        idx = torch.tensor(self.key_rows(), device=evk.data.device)
+        return evk.data.index_select(2, idx).contiguous()
+
+    def shard_rows(self, rows, level: int):
+        """(..., level+1, N) full rows -> (..., n_main, N) this rank's rows."""
+        import torch
+        idx = torch.tensor(self.main_rows(level), device=rows.device, dtype=torch.long)
+        return rows.index_select(rows.dim() - 2, idx).contiguous()
+
+    def workspace(self, level: int, batch: int):
+        import torch
+        key = (level, batch, torch.cuda.current_stream().cuda_stream)
+        ws = self._ws.get(key)
+        if ws is None:
+            n = self.lib.lf_shard_ws_bytes(self.handle, level, batch) // 4
+            ws = torch.empty(n, dtype=torch.int32, device="cuda")
+            self._ws[key] = ws
+        return ws
+
+    def gather_layout(self, level: int, batch: int):
+        from . import _native
+        a = (_ct.c_size_t * 6)()
+        _native.check(self.lib.lf_shard_gather_layout(self.handle, level, batch, a), "lf_shard_gather_layout")
+        return tuple(int(x) for x in a)
+
+    # calls -----------------------------------------------------------------------------
+    def _call(self, level, op, batch, x, x2, x_bs, keys, galois, out, out_bs, e0=None, e1=None, e_bs=0):
+        keys = list(keys)
+        karr = (_ct.c_void_p * batch)(*[(keys[i] if len(keys) > 1 else keys[0]).data_ptr() for i in range(batch)])
+        garr = (_ct.c_uint32 * batch)(*[int(g) & 0xFFFFFFFF for g in galois]) if galois is not None else None
+        c = _ShardCall(level, op, batch, x.data_ptr() if x is not None else None,
+                       x2.data_ptr() if x2 is not None else None, x_bs, _ct.cast(karr, _ct.c_void_p),
+                       _ct.cast(garr, _ct.c_void_p) if garr is not None else None,
+                       out.data_ptr() if out is not None else None, out_bs,
+                       e0.data_ptr() if e0 is not None else None, e1.data_ptr() if e1 is not None else None, e_bs)
+        # the call holds raw pointers: keep every operand alive as long as the call object
+        return c, (karr, garr, x, x2, keys, out, e0, e1)
+
+    def run(self, call, level, batch):
+        from . import _native
+        from .context import stream_handle
+        if self.comm is not None and not isinstance(self.comm, NcclComm):
+            return self._run_torch(call, level, batch)
+        c, keep = call
+        ws = self.workspace(level, batch)
+        _native.check(self.lib.lf_shard_keyswitch(self.handle, _ct.byref(c), _ct.c_void_p(ws.data_ptr()),
+                                                  stream_handle()), "lf_shard_keyswitch")
+
+    def _run_torch(self, call, level, batch):
+        """Phases 0-2 with the two all-gathers through torch.distributed (fixed sizes, no size
+        exchange, no host synchronisation with NCCL; gloo copies through host memory)."""
+        import torch
+        import torch.distributed as dist
+        group = None if self.comm == "torch" else self.comm
+        ws = self.workspace(level, batch).view(torch.uint8)
+        lay = self.gather_layout(level, batch)
+        nccl = dist.get_backend(group) == "nccl"
+        for p, (so, nb, ro) in ((0, lay[:3]), (1, lay[3:])):
+            self.phase(p, call, level, batch)
+            send, recv = ws[so: so + nb], ws[ro: ro + self.k * nb]
+            if nccl:
+                dist.all_gather_into_tensor(recv, send, group=group)
+            else:
+                parts = [torch.empty(nb, dtype=torch.uint8) for _ in range(self.k)]
+                dist.all_gather(parts, send.cpu(), group=group)
+                recv.copy_(torch.cat(parts))
+        self.phase(2, call, level, batch)
+
+    def phase(self, p, call, level, batch):
+        from . import _native
+        from .context import stream_handle
+        c, keep = call
+        ws = self.workspace(level, batch)
+        _native.check(self.lib.lf_shard_ks_phase(self.handle, p, _ct.byref(c), _ct.c_void_p(ws.data_ptr()),
+                                                 stream_handle()), "lf_shard_ks_phase")
+
+    def keyswitch_call(self, level, x_loc, key_loc, out=None):
+        """x_loc: (B, n_main, N) this rank's rows -> out (B, 2, n_main, N): (ks_b, ks_a)."""
+        import torch
+        B, nm = x_loc.shape[0], x_loc.shape[1]
+        out = torch.empty((B, 2, nm, self.params.N), dtype=torch.int32, device="cuda") if out is None else out
+        return self._call(level, OP_KS, B, x_loc, None, x_loc[0].numel(), [key_loc], None, out,
+                          out[0].numel()), out
+
+    def hom_mul_call(self, level, ct1_loc, ct2_loc, rlk_loc, out=None):
+        """ct*_loc: (B, 2, n_main, N) local blocks -> relinearised product (B, 2, n_main, N)."""
+        import torch
+        out = torch.empty_like(ct1_loc) if out is None else out
+        return self._call(level, OP_MUL, ct1_loc.shape[0], ct1_loc[:, 1], ct2_loc[:, 1], ct1_loc[0].numel(),
+                          [rlk_loc], None, out, out[0].numel(), ct1_loc, ct2_loc, ct1_loc[0].numel()), out
+
+    def rotate_call(self, level, ct_loc, gs, keys_loc, out=None):
+        """ct_loc: (B, 2, n_main, N) -> B rotations (Galois element gs[b], key keys_loc[b])."""
+        import torch
+        out = torch.empty_like(ct_loc) if out is None else out
+        return self._call(level, OP_ROT, ct_loc.shape[0], ct_loc[:, 1], None, ct_loc[0].numel(), keys_loc,
+                          list(gs), out, out[0].numel(), ct_loc, None, ct_loc[0].numel()), out
+
+    def keyswitch(self, level, x_loc, key_loc):
+        call, out = self.keyswitch_call(level, x_loc, key_loc)
+        self.run(call, level, x_loc.shape[0])
+        return out
+
+    def hom_mul(self, level, ct1_loc, ct2_loc, rlk_loc):
+        call, out = self.hom_mul_call(level, ct1_loc, ct2_loc, rlk_loc)
+        self.run(call, level, ct1_loc.shape[0])
+        return out
+
+    def rotate(self, level, ct_loc, gs, keys_loc):
+        call, out = self.rotate_call(level, ct_loc, gs, keys_loc)
+        self.run(call, level, ct_loc.shape[0])
+        return out
+
+
+def emulate(engines, calls, level: int, batch: int):
+    """Run k ranks' sharded pipelines in ONE process on one device: each rank's phases on its
+    own workspace, the two all-gathers as device copies (what ncclAllGather moves over NVLink).
+    Tests the sharded data layout and kernels without k GPUs."""
+    import torch
+    k = len(engines)
+    lays = [e.gather_layout(level, batch) for e in engines]
+    wss = [e.workspace(level, batch).view(torch.uint8) for e in engines]
+
+    def gather(send_off, nbytes, recv_off):
+        for r in range(k):
+            for src in range(k):
+                wss[r][recv_off[r] + src * nbytes: recv_off[r] + (src + 1) * nbytes].copy_(
+                    wss[src][send_off[src]: send_off[src] + nbytes])
+    for e, c in zip(engines, calls):
+        e.phase(0, c, level, batch)
+    gather([l[0] for l in lays], lays[0][1], [l[2] for l in lays])
+    for e, c in zip(engines, calls):
+        e.phase(1, c, level, batch)
+    gather([l[3] for l in lays], lays[0][4], [l[5] for l in lays])
+    for e, c in zip(engines, calls):
+        e.phase(2, c, level, batch)

@@ -110,6 +110,13 @@ def _gpu_worker(rank, world, port, outdir):
             out[f"{name}_{g}_b"] = b.cpu().numpy()
             out[f"{name}_{g}_a"] = a.cpu().numpy()
         out[f"{name}_ids"] = np.array(lay.main_loc)
+        # the fused sharded pipeline (lf_shard_*), gathers through torch.distributed (gloo here)
+        from paper_2512_11269_b200.shard import ShardEngine
+        e = ShardEngine(p, world, rank, comm="torch")
+        assert e.main_rows(level) == list(lay.main_loc)
+        o = e.keyswitch(level, x_loc[None].contiguous(), e.shard_key(rlk))
+        out[f"{name}_fused_b"] = o[0, 0].cpu().numpy()
+        out[f"{name}_fused_a"] = o[0, 1].cpu().numpy()
     np.savez(os.path.join(outdir, f"g{rank}.npz"), **out)
     dist.destroy_process_group()
 
@@ -147,3 +154,6 @@ def test_sharded_keyswitch_gpu_two_ranks(tmp_path):
                 for i, bid in enumerate(z[f"{name}_ids"]):
                     assert np.array_equal(z[f"{name}_{g}_b"][i].view(np.uint32), wb[bid].astype(np.uint32)), (name, g, bid)
                     assert np.array_equal(z[f"{name}_{g}_a"][i].view(np.uint32), wa[bid].astype(np.uint32)), (name, g, bid)
+                    if g is None:
+                        assert np.array_equal(z[f"{name}_fused_b"][i].view(np.uint32), wb[bid].astype(np.uint32))
+                        assert np.array_equal(z[f"{name}_fused_a"][i].view(np.uint32), wa[bid].astype(np.uint32))
