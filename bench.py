@@ -360,39 +360,6 @@ def ntt_throughput(params, dev, rows=720, reps=10):
     return out
 
 
-def sharded_keyswitch_latency(params, level, rlk, rank, world, dev, reps=10):
-    """one C2 keyswitch limb-sharded over all ranks (row bid on rank bid % k; one
-    all-gather before the ModUp base conversion, one before ModDown).  Latency = max over ranks
-    of the CUDA-event time of `reps` back-to-back sharded keyswitches (barrier on both sides)."""
-    import torch
-    import torch.distributed as dist
-    from paper_2512_11269_b200.shard import Layout, TorchComm, gpu_sharded_keyswitch
-    comm = TorchComm()
-    lay = Layout(level, params.num_special, params.ks.d, world, rank)
-    q = torch.tensor([params.rns_basis[i] for i in lay.main_loc], dtype=torch.int64, device=dev)[:, None]
-    g = torch.Generator(device=dev).manual_seed(99)
-    x_loc = (torch.randint(0, 2 ** 62, (len(lay.main_loc), params.N), device=dev, generator=g,
-                           dtype=torch.int64) % q).to(torch.int32)
-    for _ in range(2):
-        gpu_sharded_keyswitch(params, level, x_loc, rlk, comm)
-    torch.cuda.synchronize()
-    dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        gpu_sharded_keyswitch(params, level, x_loc, rlk, comm)
-    b.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    bytes_gathered = (level + 1 + 2 * params.num_special) * params.N * 4
-    return {"ms_per_keyswitch": float(t.item()), "ranks": world, "backend": comm.backend,
-            "allgather_rows": level + 1 + 2 * params.num_special,
-            "allgather_bytes_total": bytes_gathered,
-            "path": "shard.gpu_sharded_keyswitch (row kernels + 2 all-gathers; not the fused pipeline)"}
-
-
 def batch_sweep(params, level, rlk, dev, batches=(1, 8), steps=5):
     """Per-keyswitch time at other batch sizes of SURVEY §8d C2 (B in {1, 8, 32}): same
     synthetic inputs, L2 flushed between steps, CUDA events."""
@@ -525,6 +492,42 @@ def secondary_keyswitch(dev, B=32, steps=5):
             "hbm_gbs": rows_alg * N * 4 / (us * 1e-6) / 1e9}
 
 
+def shard_emulation(params, level, rlk, dev, batch=32, ks=(2, 4, 8), reps=3):
+    """SURVEY §8e on ONE GPU: the limb-sharded pipeline of k ranks run rank by rank (each rank's
+    rows and key rows, the gathers as device copies): per-rank device time of its three phases
+    (CUDA events, max over ranks) per keyswitch, next to the single-device pipeline.  The NVLink
+    all-gathers are NOT measured here (one GPU); their bytes are reported."""
+    import torch
+    from paper_2512_11269_b200.shard import ShardEngine
+    l1, N = level + 1, params.N
+    q = torch.tensor(params.rns_basis[:l1], dtype=torch.int64, device=dev)[:, None]
+    g = torch.Generator(device=dev).manual_seed(9)
+    xs = (torch.randint(0, 2 ** 62, (batch, l1, N), device=dev, generator=g, dtype=torch.int64) % q).to(torch.int32)
+    out = {}
+    for k in ks:
+        eng = [ShardEngine(params, k, r) for r in range(k)]
+        calls = [e.keyswitch_call(level, e.shard_rows(xs, level), e.shard_key(rlk))[0] for e in eng]
+        per = [0.0] * k
+        for it in range(reps + 1):
+            for r, (e, c) in enumerate(zip(eng, calls)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for ph in range(3):
+                    e.phase(ph, c, level, batch)
+                b.record()
+                torch.cuda.synchronize()
+                if it:
+                    per[r] += a.elapsed_time(b) / reps
+        lay = eng[0].gather_layout(level, batch)
+        out[str(k)] = {"per_rank_compute_us_per_keyswitch": max(per) / batch * 1e3,
+                       "ranks_us": [x / batch * 1e3 for x in per],
+                       "allgather_bytes_per_rank_per_keyswitch": (lay[1] + lay[4]) / batch,
+                       "key_rows_per_gpu": eng[0].info(params.max_level)["n_key_rows"]}
+        del eng, calls
+    out["note"] = "per-rank kernel time of the limb-sharded pipeline, ranks emulated one by one on one B200; gathers not timed"
+    return out
+
+
 def ntt_summary(ntt, clocks):
     mhz = (clocks or {}).get("sm_mhz") or 1965
     peak = 32 * 148 * mhz * 1e6                  # IMAD.HI per second (one per butterfly)
@@ -533,6 +536,118 @@ def ntt_summary(ntt, clocks):
     ntt["config"] = "720 rows x 2^16, C2 primes, lf_ntt_fwd / lf_ntt_inv (column + row pass)"
     ntt["int_peak"] = f"32 IMAD.HI/clk/SM x 148 SMs x {mhz} MHz (measured rate, profiles/r01_ubench_imad.log)"
     return ntt
+
+
+def run_sharded(args, rank, world):
+    """N > 1: every C2 keyswitch of the step is LIMB-SHARDED over all ranks
+    (main row i and special row j on rank i % k / j % k, multidev.py:55-56); each rank runs
+    the fused pipeline on its rows with its rows of the key (1/k of the key resident) and the
+    two all-gathers go through the library's own NCCL communicator on the launch stream
+    (lf_shard_keyswitch).  The total work per step is fixed (B keyswitches), so `scaling` is
+    "strong"; independent per-GPU replicas (weak scaling) are reported beside it."""
+    import torch
+    import torch.distributed as dist
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.context import get_context
+    from paper_2512_11269_b200.shard import NcclComm, ShardEngine
+    dev = torch.device("cuda", torch.cuda.current_device())
+    params = B.gen_params(**C2)
+    level, N, Bsz = args.level, params.N, args.batch
+    l1 = level + 1
+    sk, pk, rlk = B.keygen(params, seed=11)           # same seed on every rank: the same key
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    q = torch.tensor(params.rns_basis[:l1], dtype=torch.int64, device=dev)[:, None]
+    g = torch.Generator(device=dev).manual_seed(1234)                   # same inputs on every rank
+    xs = [((torch.randint(0, 2 ** 62, (Bsz, l1, N), device=dev, generator=g, dtype=torch.int64) % q)
+           .to(torch.int32)) for _ in range(3)]
+
+    def timed(fn, steps):
+        for i in range(args.warmup):
+            fn(i)
+        torch.cuda.synchronize()
+        dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            flush.fill_(i)
+            evs[i][0].record(stream)
+            fn(i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # replicas (weak scaling): every rank keyswitches its own batch with the full key
+    ws = get_context(params).ks_workspace(level, Bsz)
+    out_full = torch.empty((Bsz, 2, l1, N), dtype=torch.int32, device=dev)
+    ms_rep = timed(lambda i: fused.keyswitch_batch(params, level, xs[i % 3], rlk, out=out_full, ws=ws), args.steps)
+    del ws, out_full
+
+    # limb-sharded (strong scaling)
+    comm_kind = "library NCCL communicator (lf_comm_create, ncclAllGather on the launch stream)"
+    try:
+        comm = NcclComm(world, rank) if dist.get_backend() == "nccl" else "torch"
+        if comm == "torch":
+            comm_kind = f"torch.distributed all_gather ({dist.get_backend()})"
+    except Exception as e:                                               # noqa: BLE001
+        comm, comm_kind = "torch", f"torch.distributed all_gather (library NCCL unavailable: {e})"
+    eng = ShardEngine(params, world, rank, comm)
+    key_loc = eng.shard_key(rlk)
+    key_bytes_full = rlk.data.numel() * 4
+    del rlk
+    torch.cuda.empty_cache()
+    xs_loc = [eng.shard_rows(x, level) for x in xs]
+    nm = xs_loc[0].shape[1]
+    out = torch.empty((Bsz, 2, nm, N), dtype=torch.int32, device=dev)
+    calls = [eng.keyswitch_call(level, x, key_loc, out=out)[0] for x in xs_loc]
+    clk = ClockSampler(torch.cuda.current_device()).start()
+    ms = timed(lambda i: eng.run(calls[i % 3], level, Bsz), args.steps)
+    clocks = clk.stop()
+    value = Bsz * args.steps / (ms / 1e3)
+
+    # batch-1 latency of one sharded keyswitch
+    one = eng.keyswitch_call(level, xs_loc[0][:1].contiguous(), key_loc)[0]
+    ms1 = timed(lambda i: eng.run(one, level, 1), 10) / 10
+
+    # e2e: each rank's rows from pinned host memory, sharded keyswitch, results back
+    h_in = torch.empty((Bsz, nm, N), dtype=torch.int32, pin_memory=True)
+    h_in.copy_(xs_loc[0].cpu())
+    h_out = torch.empty((Bsz, 2, nm, N), dtype=torch.int32, pin_memory=True)
+    d_in = torch.empty_like(xs_loc[0])
+    ecall = eng.keyswitch_call(level, d_in, key_loc, out=out)[0]
+
+    def e2e(i):
+        d_in.copy_(h_in, non_blocking=True)
+        eng.run(ecall, level, Bsz)
+        h_out.copy_(out, non_blocking=True)
+    ms_e2e = timed(e2e, args.steps)
+    if rank == 0:
+        lay = eng.gather_layout(level, Bsz)
+        line = {
+            "metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "C2 full-level hybrid keyswitch, N=2^16, L=35, dnum=4, alpha=9",
+                       "level": level, "batch_per_step": Bsz, "parallelism": f"limb-sharded{world}",
+                       "l2": "256 MB flush between timed steps; inputs cycled over 3 batches"},
+            "keyswitch_us": ms / args.steps / Bsz * 1e3,
+            "limb_sharded": {"latency_batch1_us": ms1 * 1e3, "comm": comm_kind,
+                             "allgather_bytes_per_rank_per_step": lay[1] + lay[4],
+                             "key_bytes_per_gpu": key_loc.numel() * 4, "key_bytes_full": key_bytes_full,
+                             "main_rows_rank0": nm},
+            "replicas": {"value": world * Bsz * args.steps / (ms_rep / 1e3), "unit": "ops/s", "scaling": "weak",
+                         "note": "every GPU keyswitches its own batch with the full key"},
+            "gpu_launches": 5 * args.steps,
+            "e2e": {"value": Bsz * args.steps / (ms_e2e / 1e3), "unit": "ops/s",
+                    "h2d_bytes_per_step": Bsz * nm * N * 4 * world, "d2h_bytes_per_step": Bsz * 2 * nm * N * 4 * world,
+                    "api": "ShardEngine.keyswitch per rank: local rows H2D, sharded pipeline, local results D2H"},
+            "clocks": clocks, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
 
 
 def run_ours(args, rank, world):
@@ -704,9 +819,7 @@ def run_ours(args, rank, world):
     rot = rotation_units(params, level, dev) if rank == 0 else None
     sec = secondary_keyswitch(dev) if rank == 0 else None
 
-    sharded = None
-    if world > 1:
-        sharded = sharded_keyswitch_latency(params, level, rlk, rank, world, dev)
+    sharded = shard_emulation(params, level, rlk, dev) if rank == 0 and world == 1 else None
 
     boot = None
     if rank == 0 and world == 1 and not args.no_bootstrap:
@@ -754,7 +867,7 @@ def run_ours(args, rank, world):
             "batch_sweep": sweep,
             "rotation": rot,
             "secondary_c2": sec,
-            "limb_sharded": sharded,
+            "limb_sharded_emulated": sharded,
         }
         print(json.dumps(line), flush=True)
 
@@ -769,6 +882,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-bootstrap", action="store_true", help="skip the C3 bootstrap latency")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of limb sharding")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -785,7 +899,10 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    run_ours(args, rank, world)
+    if world > 1 and not args.replicas:
+        run_sharded(args, rank, world)
+    else:
+        run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
