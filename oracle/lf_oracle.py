@@ -441,7 +441,7 @@ def encode(values, P: Params, level=None, scale=None) -> Plain:
     Qp = 1
     for q in P.main[:level + 1]:
         Qp *= q
-    if np.abs(r).max(initial=0.0) >= Qp // 4:
+    if int(np.abs(r).max(initial=0.0)) >= Qp // 4:     # exact: Qp can exceed the float range
         raise OverflowError("ScaleOverflow")
     ints = r.astype(np.int64)
     rows = np.stack([ntt_fwd(np.mod(ints, q).astype(U64), q) for q in P.main[:level + 1]])

@@ -306,11 +306,15 @@ def evalmod_plain(x: np.ndarray, cfg: BootConfig) -> np.ndarray:
 # the algorithm over a backend
 # ---------------------------------------------------------------------------------------
 
-class Bootstrapper:
-    """Precomputes the plaintext diagonals of CoeffToSlot / SlotToCoeff for `params` and runs
-    the pipeline over `backend` (GpuBackend for the product)."""
+class CkksCircuit:
+    """Scale / level bookkeeping and the homomorphic building blocks shared by the bootstrap
+    and the encrypted layer workloads (workloads.py): BSGS linear maps with hoisted rotations
+    (`_linear`), exact scale matching (`_match`), relinearised products with the double-prime
+    rescale (`_mul2`), and Chebyshev-basis polynomial evaluation (`_cheb_powers`,
+    `_cheb_eval`).  Everything is written against a backend (GpuBackend for the product, the
+    oracle backend in tests), so each composition is checked residue for residue."""
 
-    def __init__(self, backend, cfg: BootConfig = BootConfig()):
+    def __init__(self, backend, cfg):
         self.be = backend
         self.cfg = cfg
         self.N = backend.N
@@ -318,40 +322,8 @@ class Bootstrapper:
         self.q = list(backend.main_primes)
         self.L = len(self.q) - 1
         self.q0 = self.q[0]
-        self.alpha, self.beta, self.cheb, self.dbl = evalmod_constants(cfg)
         self.out_scale = Fraction(getattr(backend, "default_scale", 1 << 26))
-        self._build_linear()
-
-    # -- planning --------------------------------------------------------------------
-    def _build_linear(self):
-        cfg, n = self.cfg, self.n
-        cts = cts_matrices(self.N, cfg.cts_levels)
-        stc = stc_matrices(self.N, cfg.stc_levels)
-        # fold alpha * (q-relative) constants: CtS output y = alpha/2 * (t_k + i t_{k+n}) / q0
-        # given input slots z = Embed(t)/Delta_in; Delta_in varies, so the factor Delta_in/q0
-        # is applied through the declared scale (see bootstrap()).  Balance the magnitude over
-        # the levels so every diagonal is O(1) (plaintext precision).
-        ratio = cfg.bsgs_ratio if cfg.lazy_moddown else 1
-        self.cts_plans = [bsgs_plan(M, n, ratio) for M in cts]
-        self.stc_plans = [bsgs_plan(M, n, ratio) for M in stc]
-        self.cts_const = self.alpha / 2
-        self.rotations = set()
-        for pl in self.cts_plans + self.stc_plans:
-            self.rotations |= pl.rotations()
-        # level schedule
-        l = self.L
-        self.cts_at = []
-        for i in range(cfg.cts_levels):
-            self.cts_at.append(l)
-            l -= 2
-        self.evalmod_in = l
         self._pt_cache = {}
-
-    def required_rotations(self) -> list:
-        return sorted(self.rotations)
-
-    def levels_used(self) -> dict:
-        return {"cts": self.cts_at, "evalmod_in": self.evalmod_in}
 
     # -- helpers ---------------------------------------------------------------------
     def _pt(self, key, vec, level, scale, ext=False):
@@ -432,10 +404,12 @@ class Bootstrapper:
             return be.mul_rescale2(a, b)
         return be.rescale2(be.hom_mul(a, b))
 
-    def _cheb_powers(self, u):
+    def _cheb_powers(self, u, degree=None):
+        """T_1..T_(baby-1) and the giant powers T_baby, T_2baby, ... up to `degree`."""
         be = self.be
         T = {1: u}
         g = self.cfg.baby
+        degree = self.cfg.cheb_degree if degree is None else degree
 
         def twice(x):
             # 2x: the same residues at half the declared scale (free) while the scale stays
@@ -456,7 +430,7 @@ class Bootstrapper:
         for m in range(2, g):
             T[m] = double(m // 2) if m % 2 == 0 else odd(m // 2)
         G = g
-        while G <= self.cfg.cheb_degree:
+        while G <= degree:
             T[G] = double(G // 2)
             G *= 2
         return T
@@ -513,6 +487,47 @@ class Bootstrapper:
         assert prod.level == level and prod.scale == scale
         rc = self._cheb_eval(r, T, level, scale)
         return be.add(prod, rc)
+
+
+class Bootstrapper(CkksCircuit):
+    """Precomputes the plaintext diagonals of CoeffToSlot / SlotToCoeff for `params` and runs
+    the pipeline over `backend` (GpuBackend for the product)."""
+
+    def __init__(self, backend, cfg: BootConfig = BootConfig()):
+        super().__init__(backend, cfg)
+        self.alpha, self.beta, self.cheb, self.dbl = evalmod_constants(cfg)
+        self._build_linear()
+
+    # -- planning --------------------------------------------------------------------
+    def _build_linear(self):
+        cfg, n = self.cfg, self.n
+        cts = cts_matrices(self.N, cfg.cts_levels)
+        stc = stc_matrices(self.N, cfg.stc_levels)
+        # fold alpha * (q-relative) constants: CtS output y = alpha/2 * (t_k + i t_{k+n}) / q0
+        # given input slots z = Embed(t)/Delta_in; Delta_in varies, so the factor Delta_in/q0
+        # is applied through the declared scale (see bootstrap()).  Balance the magnitude over
+        # the levels so every diagonal is O(1) (plaintext precision).
+        ratio = cfg.bsgs_ratio if cfg.lazy_moddown else 1
+        self.cts_plans = [bsgs_plan(M, n, ratio) for M in cts]
+        self.stc_plans = [bsgs_plan(M, n, ratio) for M in stc]
+        self.cts_const = self.alpha / 2
+        self.rotations = set()
+        for pl in self.cts_plans + self.stc_plans:
+            self.rotations |= pl.rotations()
+        # level schedule
+        l = self.L
+        self.cts_at = []
+        for i in range(cfg.cts_levels):
+            self.cts_at.append(l)
+            l -= 2
+        self.evalmod_in = l
+        self._pt_cache = {}
+
+    def required_rotations(self) -> list:
+        return sorted(self.rotations)
+
+    def levels_used(self) -> dict:
+        return {"cts": self.cts_at, "evalmod_in": self.evalmod_in}
 
     def _evalmod(self, x):
         """x: slots in [-K, K] (already u = alpha x + beta) -> sin(2 pi x)/(2 pi)."""
@@ -796,6 +811,28 @@ class GpuBackend:
         every giant step's plaintext sum in one lf_bsgs_ext pipeline, then one batched
         mod_down and the giant rotations (rotate_and_sum).  None when the plan exceeds the
         kernel's limits (the caller then composes the unfused primitives)."""
+        import torch
+        n = self.params.n
+        rot = sorted({b for _, pairs in groups for b, _ in pairs if b % n})
+        G = len(groups)
+        if not rot or len(rot) > 32 or not self.permuted_keys:
+            return None
+        if G > 4:
+            # more giant steps than one k_bsgs_ext holds: chunks of 4 giants (each chunk reruns
+            # the hoisted ModUp and its baby rotations), then ONE batched mod_down of all giants
+            chunks = [groups[i: i + 4] for i in range(0, G, 4)]
+            if any(not any(b % n for _, prs in c for b, _ in prs) for c in chunks):
+                return None
+            inner = [self._bsgs_inner(ct, c) for c in chunks]
+            pt0 = groups[0][1][0][1]
+            return self._moddown_and_sum(torch.cat(inner), [st for st, _ in groups], ct.scale * pt0.scale,
+                                         ct.level)
+        inner = self._bsgs_inner(ct, groups)
+        pt0 = next(pt for _, pairs in groups for _, pt in pairs)
+        return self._moddown_and_sum(inner, [st for st, _ in groups], ct.scale * pt0.scale, ct.level)
+
+    def _bsgs_inner(self, ct, groups):
+        """lf_bsgs_ext for <= 4 giant groups: (G, 2, ext, N) extended-basis giant sums."""
         import ctypes
         import torch
         from . import _native
@@ -804,8 +841,6 @@ class GpuBackend:
         n = self.params.n
         rot = sorted({b for _, pairs in groups for b, _ in pairs if b % n})
         G = len(groups)
-        if not rot or len(rot) > 32 or G > 4 or not self.permuted_keys:
-            return None
         slot = {b: 1 + i for i, b in enumerate(rot)}
         ctx = get_context(self.params)
         lib = _native.lib()
@@ -827,7 +862,7 @@ class GpuBackend:
         inner = torch.empty((G, 2, ext, N), dtype=torch.int32, device="cuda")
         _native.check(lib.lf_bsgs_ext(ctx.handle, level, dptr(ct_block(ct)), len(rot), _native.u32_array(gs),
                                       karr, G, parr, dptr(inner), dptr(ws), stream_handle()), "lf_bsgs_ext")
-        return self._moddown_and_sum(inner, [st for st, _ in groups], ct.scale * pt0.scale, level)
+        return inner
 
     def _moddown_and_sum(self, inner, shifts, scale, level):
         """ONE batched mod_down of the giant steps' extended sums (lf_moddown_ext), then the
