@@ -24,6 +24,7 @@ import sys
 import time
 
 import numpy as np
+from fractions import Fraction
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -328,6 +329,125 @@ def bootstrap_latency(reps=5):
             "levels": f"in 0 -> out {gout.level} (L=47)", "precision_bits": -np.log2(err),
             "max_err_vs_plain": err_v, "rotation_keys": len(rk) + 1,
             "paper_1xB200_ms": 14.5, "setup_s": time.time() - t0}
+
+
+def _graph_latency(be, fn, ct, reps):
+    """Eager latency of fn(ct) and its CUDA-graph replay latency (median of reps), CUDA events
+    on the launch stream; the replay must equal the eager output residue for residue."""
+    import torch
+    from paper_2512_11269_b200 import bootstrap as BT
+    out = fn(ct)                                          # encodes and caches the plaintexts
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn(ct)
+    e1.record()
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1)
+    g = BT.GraphedCircuit(be, fn, ct)
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        gout = g(ct)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    assert np.array_equal(gout.b.numpy(), out.b.numpy()), "graph replay differs from eager"
+    return out, eager_ms, statistics.median(ms)
+
+
+def _workload_env(kw, rotations):
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import bootstrap as BT
+    p = B.gen_params(**kw)
+    sk, pk, rlk = B.keygen(p, seed=11)
+    ck, rk = BT.make_bootstrap_keys(p, sk, rotations, seed=99)
+    return p, sk, pk, BT.GpuBackend(p, rlk, ck, rk), len(rk)
+
+
+class _Planner:
+    def __init__(self, kw):
+        import paper_2512_11269_b200 as B
+        self.N = kw["N"]
+        self.main_primes = B.gen_params(**kw).rns_basis
+
+
+C4_SHAPE = (16, 32, 32)          # ResNet-20 stage 1 on CIFAR-10: 16 channels, 32 x 32
+
+
+def resnet_block_latency(reps=3):
+    """C4 (BASELINE config 4): one ResNet-20 basic block relu(conv2(relu(conv1 x)) + x) on a
+    16 x 32 x 32 activation (CIFAR-10 stage 1, slots c*1024 + y*32 + x, replicated 2x in
+    n = 2^15), conv3x3 as a hoisted BSGS rotate-and-sum over the C*9 = 144 diagonals
+    (workloads.ResNetBlock), degree-15 Chebyshev ReLU, at the C3 parameters from level 47.
+    Weights default_rng(5) uniform(-1,1)/(9C); CUDA graph replay."""
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import workloads as WL
+    t0 = time.time()
+    C = C4_SHAPE[0]
+    rng = np.random.default_rng(5)
+    w1 = rng.uniform(-1, 1, (C, C, 3, 3)) / (9 * C)
+    w2 = rng.uniform(-1, 1, (C, C, 3, 3)) / (9 * C)
+    rots = WL.ResNetBlock(_Planner(C3), w1, w2, C4_SHAPE).required_rotations()
+    p, sk, pk, be, nkeys = _workload_env(C3, rots)
+    blk = WL.ResNetBlock(be, w1, w2, C4_SHAPE)
+    act = np.random.default_rng(7).uniform(-1, 1, C4_SHAPE) * 0.5
+    S = Fraction(p.rns_basis[p.max_level]) * p.rns_basis[p.max_level - 1]
+    ct = B.encrypt(B.encode(blk.pack(act), p, level=p.max_level, scale=S), pk, p, np.random.default_rng(5))
+    setup = time.time() - t0
+    out, eager_ms, ms = _graph_latency(be, blk.forward, ct, reps)
+    got = B.decrypt(out, sk, p)[: act.size].real
+    err_model = float(np.abs(got - blk.plain(blk.pack(act))[: act.size]).max())
+    err_true = float(np.abs(got - blk.reference(act).reshape(-1)).max())
+    return {"ms": ms, "ms_eager": eager_ms, "reps": reps,
+            "workload": "ResNet-20 basic block, 16x32x32 activation, two conv3x3 (144 diagonals, "
+                        "BSGS 9 baby x 17 giant, hoisted) + two degree-15 Chebyshev ReLU + shortcut",
+            "params": "gen_params(65536, 47, d=4, scale=2^26), h=64", "levels": f"47 -> {out.level}",
+            "rotation_keys": nkeys, "max_err_vs_slot_model": err_model, "max_err_vs_network": err_true,
+            "paper_context": "full ResNet-20 (9 blocks + bootstraps) 456 ms on 1xB200 (PAPER.md:688)",
+            "setup_s": setup}
+
+
+C5 = dict(N=65536, num_levels=52, d=4, seed=0, scale=2 ** 26)
+C5_SHAPE = (128, 64)             # BERT-Base: 128 tokens, head dimension 64
+
+
+def transformer_block_latency(reps=2):
+    """C5 (BASELINE config 5): one single-head transformer block over T = 128 tokens x d = 64
+    features (BERT-Base sequence length and head dimension; rows packed row-major, replicated
+    4x): Q/K/V/O and two FFN projections as BSGS mat-vecs of I_T (x) W (127 diagonals), scores
+    for all 128 offsets as ciphertext products + rotate-and-sum, softmax as Chebyshev exp and
+    1/x, GELU as the reference's least-squares fit (workloads.TransformerBlock), at
+    gen_params(65536, 52, d=4) from level 52 (the block uses 50 levels).  Weights
+    default_rng(5) uniform(-1,1)/d; one GPU, CUDA graph replay."""
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import workloads as WL
+    t0 = time.time()
+    T, d = C5_SHAPE
+    rng = np.random.default_rng(5)
+    Ws = [rng.uniform(-1, 1, (d, d)) / d for _ in range(6)]
+    kw = dict(T=T, d=d, score_bound=1.0, gelu_bound=2.0)
+    rots = WL.TransformerBlock(_Planner(C5), *Ws, **kw).required_rotations()
+    p, sk, pk, be, nkeys = _workload_env(C5, rots)
+    blk = WL.TransformerBlock(be, *Ws, **kw)
+    X = np.random.default_rng(8).uniform(-1, 1, (T, d)) * 0.5
+    S = Fraction(p.rns_basis[p.max_level]) * p.rns_basis[p.max_level - 1]
+    ct = B.encrypt(B.encode(blk.pack(X), p, level=p.max_level, scale=S), pk, p, np.random.default_rng(6))
+    setup = time.time() - t0
+    out, eager_ms, ms = _graph_latency(be, blk.forward, ct, reps)
+    got = B.decrypt(out, sk, p)[: T * d].real.reshape(T, d)
+    err = float(np.abs(got - blk.reference(X)).max())
+    key_gb = nkeys * 2 * p.ks.d * (p.max_level + 1 + p.num_special) * p.N * 4 / 1e9
+    return {"ms": ms, "ms_eager": eager_ms, "reps": reps,
+            "workload": "single-head transformer block, 128 tokens x 64 features: 6 BSGS projections, "
+                        "128-offset attention scores, Chebyshev exp + 1/x softmax, GELU lsq fit",
+            "params": "gen_params(65536, 52, d=4, scale=2^26), h=64", "levels": f"52 -> {out.level}",
+            "rotation_keys": nkeys, "key_gb_per_gpu_1": key_gb,
+            "key_gb_per_gpu_sharded_8": key_gb / 8,
+            "max_err_vs_float_block": err,
+            "paper_context": "full BERT-Base (12 layers x 12 heads, 768 hidden) 28.3 s on 1xB200 (PAPER.md:695)",
+            "setup_s": setup}
 
 
 def ntt_throughput(params, dev, rows=720, reps=10):
@@ -827,6 +947,16 @@ def run_ours(args, rank, world):
         torch.cuda.empty_cache()
         boot = bootstrap_latency()
 
+    layers = None
+    if rank == 0 and world == 1 and not args.no_workloads:
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        layers = {"resnet_block": resnet_block_latency()}
+        gc.collect()
+        torch.cuda.empty_cache()
+        layers["transformer_block"] = transformer_block_latency()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world,
@@ -868,6 +998,7 @@ def run_ours(args, rank, world):
             "rotation": rot,
             "secondary_c2": sec,
             "limb_sharded_emulated": sharded,
+            "layers": layers,
         }
         print(json.dumps(line), flush=True)
 
@@ -882,6 +1013,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-bootstrap", action="store_true", help="skip the C3 bootstrap latency")
+    ap.add_argument("--no-workloads", action="store_true", help="skip the C4/C5 layer latencies")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of limb sharding")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

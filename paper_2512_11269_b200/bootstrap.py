@@ -1265,43 +1265,53 @@ def make_bootstrap_keys(params, sk, rotations, seed: int = 99):
     return ck, rk
 
 
-class GraphedBootstrap:
-    """A Bootstrapper captured once as a CUDA graph (the paper's runtime also replays CUDA
-    graphs).  Every kernel of the pipeline, with its workspace and the resident
-    plaintext diagonals and keys, is recorded on the first call; later calls copy the input
-    ciphertext into the captured input buffers and replay.  Inputs must share the captured
-    ciphertext's level-0 scale (the diagonals fold Delta_in in)."""
+class GraphedCircuit:
+    """A circuit `fn(ct) -> ct` over a GpuBackend captured once as a CUDA graph (the paper's
+    runtime also replays CUDA graphs).  Every kernel, with its workspace and the
+    resident plaintexts and keys, is recorded on the first call; later calls copy the input
+    ciphertext into the captured input buffers and replay.  Inputs must arrive at the captured
+    level and scale (plaintext constants are encoded against them)."""
 
-    def __init__(self, bootstrapper: Bootstrapper, example_ct):
+    def __init__(self, backend, fn, example_ct, level=None):
         import torch
         from .ckks import Ciphertext
         from .poly import RnsPolynomial
-        self.bt = bootstrapper
-        ct0 = bootstrapper.be.drop_to_level(example_ct, 0)
+        self.be, self.fn = backend, fn
+        self.level = example_ct.level if level is None else level
+        ct0 = backend.drop_to_level(example_ct, self.level)
         self.scale = ct0.scale
         self._in = torch.stack([ct0.b.limbs.clone(), ct0.a.limbs.clone()])
         ids = ct0.b.basis_ids
         self._ct = Ciphertext(RnsPolynomial(self._in[0], ct0.b.domain, ids),
-                              RnsPolynomial(self._in[1], ct0.a.domain, ids), ct0.scale, 0)
-        bootstrapper.bootstrap(self._ct)                 # encode / cache every plaintext
+                              RnsPolynomial(self._in[1], ct0.a.domain, ids), ct0.scale, self.level)
+        fn(self._ct)                                     # encode / cache every plaintext
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            bootstrapper.bootstrap(self._ct)             # warm the allocator pool
+            fn(self._ct)                                 # warm the allocator pool
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self._out = bootstrapper.bootstrap(self._ct)
+            self._out = fn(self._ct)
 
     def __call__(self, ct):
         from .ckks import Ciphertext
         from .poly import RnsPolynomial
-        ct0 = self.bt.be.drop_to_level(ct, 0)
+        ct0 = self.be.drop_to_level(ct, self.level)
         if ct0.scale != self.scale:
-            raise ValueError("GraphedBootstrap: input scale differs from the captured one")
+            raise ValueError(f"{type(self).__name__}: input scale differs from the captured one")
         self._in[0].copy_(ct0.b.limbs)
         self._in[1].copy_(ct0.a.limbs)
         self.graph.replay()
         o = self._out
         return Ciphertext(RnsPolynomial(o.b.limbs.clone(), o.b.domain, o.b.basis_ids),
                           RnsPolynomial(o.a.limbs.clone(), o.a.domain, o.a.basis_ids), o.scale, o.level)
+
+
+class GraphedBootstrap(GraphedCircuit):
+    """A Bootstrapper captured once as a CUDA graph; inputs must share the captured
+    ciphertext's level-0 scale (the diagonals fold Delta_in in)."""
+
+    def __init__(self, bootstrapper: Bootstrapper, example_ct):
+        self.bt = bootstrapper
+        super().__init__(bootstrapper.be, bootstrapper.bootstrap, example_ct, level=0)
