@@ -384,6 +384,15 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 // (8 targets x 4 bytes) = 512 TMEM columns; the MMAs of round r+1 run during the NTT column
 // passes of round r.  Replaces 10 IMAD.WIDE per target element (the fmaheavy-bound part of
 // k_bconv_colpass) with ~6 ALU ops and a quarter of a tcgen05.ld.
+#ifdef LF_BC_TRACE
+// Phase timestamps of two CTAs (experiment builds only: -DLF_BC_TRACE): recorded into shared
+// memory by thread 0 of each group, printed after the kernel's work.
+#define LF_TR_ON (blockIdx.x == 0 || blockIdx.x == 2000)
+#define LF_TR(slot) do { if (LF_TR_ON && (threadIdx.x % 128) == 0 && tr_n < 48) { \
+    tr_t[threadIdx.x / 128][tr_n] = clock64(); tr_c[threadIdx.x / 128][tr_n++] = slot; } } while (0)
+#else
+#define LF_TR(slot) do {} while (0)
+#endif
 template <int L1, int L2, int KB>
 __global__ void __launch_bounds__(1024, 1)
 k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
@@ -397,8 +406,15 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   constexpr int MT = 16 * SBO;                  // bytes per M-tile (128 rows)
   constexpr int ABYTES = E * MT + 128;          // + tail met by the aliased 4th K-chunk (KB = 48)
   extern __shared__ __align__(1024) unsigned char smb[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar;                     // MMA completion of the current round
   __shared__ uint32_t tbase_s;
+  __shared__ u32 arrive_cnt;                    // warps done reading TMEM, cumulative over rounds
+  __shared__ double invs_sm[16];                // 1 / s_i of the sources (phase 2)
+#ifdef LF_BC_TRACE
+  __shared__ long long tr_t[8][48];
+  __shared__ char tr_c[8][48];
+  int tr_n = 0;
+#endif
   unsigned char* As = smb;
   unsigned char* Ws = smb + ABYTES;
   const int grp = threadIdx.x / GT, lt = threadIdx.x % GT;
@@ -435,23 +451,33 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
     uint4* wd = reinterpret_cast<uint4*>(Ws);
     for (int v = threadIdx.x; v < nz; v += blockDim.x) wd[v] = v < nw ? __ldg(wsrc + v) : make_uint4(0, 0, 0, 0);
     if (threadIdx.x < 32) tmem_alloc(&tbase_s, 512);
-    if (threadIdx.x == 0) mbar_init(&mbar, 1);
+    if (threadIdx.x == 0) {
+      mbar_init(&mbar, 1);
+      arrive_cnt = 0;
+    }
+    if (threadIdx.x < k) invs_sm[threadIdx.x] = B.inv_s[threadIdx.x];
   }
   lf_pdl_wait();
 
-  // phase 1: INTT column pass of each source, times c_i, into the A operand (rows = lanes)
+  // phase 1: INTT column pass of each source, times c_i, into the A operand (rows = lanes).
+  // (A remainder of k % 8 sources run with all 1024 threads per source, one butterfly per
+  // thread and stage through shared memory, measured slower than one group per source.)
+  LF_TR('1');
   const int cl = A.tsplit;
   for (int i = ts + cl * grp; i < k; i += cl * TG) {
     const int pi = B.src_pi[i];
     const PrimeK pk = dv.pk[pi];
     u32 x[E];
     load_col_step2<L1, L2>(x, src + ((size_t)bc_src_row(G.src_row0, G.src_rows[i], A.src_rstride) << logN) + col, tl);
+    LF_TR('l');
     inv_line<L1>(x, 1u, TwGlobalT<L1>{dv.twiT + ((size_t)pi << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
+    LF_TR('i');
     const u32 ci = B.c[i], cpi = B.cp[i];
 #pragma unroll
     for (int e = 0; e < E; ++e) *yword(e, i) = mul_shoup(x[e], ci, cpi, pk.q);
     gsync();
   }
+  LF_TR('E');
   if (cl > 1) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     for (int i = 0; i < k; ++i) {
@@ -472,21 +498,43 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   __syncthreads();
 
   // phase 2: exact overflow count u of each element (only group 0's 128 threads hold distinct
-  // rows; the 8 groups split the 16 M-tiles) -> K-row 4k of the A operand
-  for (int e = grp; e < E; e += TG) {
-    double v = 0.0;
-    for (int i = 0; i < k; ++i) v = fma((double)*yword(e, i), B.inv_s[i], v);
-    const double r = rint(v);
-    u32 uj;
-    if (fabs(v - r) >= 0x1p-40) {
-      uj = (u32)floor(v);
-    } else {
-      u32 yy[64];
-      bool z = true;
-      for (int i = 0; i < k; ++i) { yy[i] = *yword(e, i); z &= yy[i] == 0; }
-      uj = z ? 0u : bconv_u_exact(yy, B, (u32)r);
+  // rows; the 8 groups split the 16 M-tiles, two per thread) -> K-row 4k of the A operand.
+  // The two elements' fp64 sums run as independent chains over 16-byte source chunks (a
+  // quarter-warp reads 128 contiguous bytes: conflict-free); any summation order is exact here
+  // (the 2^-40 risk window dwarfs the rounding of k <= 11 terms).
+  static_assert(E == 2 * TG, "two M-tiles per thread in phase 2");
+  {
+    double v[2] = {0.0, 0.0};
+    const uint4* yc[2] = {reinterpret_cast<const uint4*>(yword(grp, 0)),
+                          reinterpret_cast<const uint4*>(yword(grp + TG, 0))};
+#pragma unroll 1
+    for (int j = 0; 4 * j < k; ++j) {
+      const uint4 a = yc[0][8 * j], b = yc[1][8 * j];
+      const u32 av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * j + q < k) {
+          const double is = invs_sm[4 * j + q];
+          v[0] = fma((double)av[q], is, v[0]);
+          v[1] = fma((double)bv[q], is, v[1]);
+        }
+      }
     }
-    *yword(e, k) = uj;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = grp + h * TG;
+      const double r = rint(v[h]);
+      u32 uj;
+      if (fabs(v[h] - r) >= 0x1p-40) {
+        uj = (u32)floor(v[h]);
+      } else {
+        u32 yy[64];
+        bool z = true;
+        for (int i = 0; i < k; ++i) { yy[i] = *yword(e, i); z &= yy[i] == 0; }
+        uj = z ? 0u : bconv_u_exact(yy, B, (u32)r);
+      }
+      *yword(e, k) = uj;
+    }
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -494,6 +542,9 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   tc_fence_after();
   const uint32_t tmem = tbase_s;
   const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(As), w0 = (uint32_t)__cvta_generic_to_shared(Ws);
+  // One MMA set per round: 8 targets x 4 byte columns (N = 32) over the 16 M-tiles.  (Two
+  // independent N = 16 sets measured slower: the tensor core re-streams the whole A operand
+  // from shared memory per MMA, so halving N doubles the operand traffic.)
   constexpr uint32_t IDESC = umma_idesc_u8(128, 32);
   auto issue = [&](int r) {
 #pragma unroll 1
@@ -504,21 +555,28 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
                 umma_sdesc(w0 + r * 2048 + 256 * s2, 128, 512), IDESC, s2 > 0);
     umma_commit(&mbar);
   };
+  LF_TR('U');
   if (threadIdx.x == 0 && nrounds > 0) issue(0);
 
   // phase 3: per round, group g takes target t0 + 8 r + g: S_b from TMEM -> X mod t (lazy) ->
-  // NTT column pass -> destination row
+  // NTT column pass -> destination row.  No CTA barrier per round: every warp, once its TMEM
+  // reads of round r completed, arrives on a shared counter (acq_rel), and the LAST warp to
+  // arrive issues the MMAs of round r + 1 into the freed accumulators, so the groups drift
+  // freely instead of waiting for the slowest one before their NTT.
   const uint32_t tlane = tmem + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) + 4 * grp;
+  const int nwarps = blockDim.x / 32;
 #pragma unroll 1
   for (int r = 0; r < nrounds; ++r) {
-    mbar_wait(&mbar, r & 1);
-    tc_fence_after();
     const int t = t0 + TG * r + grp;
     const bool active = t < t1;                          // uniform over the group's 4 warps
-    u32 x[E];
     PrimeK pk;
+    if (active) pk = dv.pk[B.tgt_pi[t]];
+    LF_TR('r');
+    mbar_wait(&mbar, r & 1);
+    tc_fence_after();
+    LF_TR('m');
+    u32 x[E];
     if (active) {
-      pk = dv.pk[B.tgt_pi[t]];
 #pragma unroll
       for (int h = 0; h < E / 4; ++h) {
         u32 s[4][4];
@@ -533,16 +591,29 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
       }
     }
     tc_fence_before();
-    __syncthreads();                                     // TMEM free for the next round
-    if (threadIdx.x == 0 && r + 1 < nrounds) {
-      tc_fence_after();
-      issue(r + 1);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const u32 old = atomic_add_acq_rel_smem(&arrive_cnt, 1u);
+      if (old == (u32)(nwarps * (r + 1) - 1) && r + 1 < nrounds) {   // last reader of round r
+        tc_fence_after();
+        issue(r + 1);
+      }
     }
+    __syncwarp();
+    LF_TR('d');
     if (active) {
       fwd_line<L1, 4>(x, 1u, TwGlobalT<L1>{dv.twfT + ((size_t)B.tgt_pi[t] << logN), 1u, 1}, pk.q, X, tl, addr, gsync);
+      LF_TR('n');
       store_col_step2<L1, L2>(x, dst + ((size_t)(G.dst_row0 + G.dst_rows[t]) << logN) + col, tl);
     }
   }
+  LF_TR('z');
+#ifdef LF_BC_TRACE
+  if (LF_TR_ON && (threadIdx.x % 128) == 0)
+    for (int i = 0; i < tr_n; ++i)
+      printf("TR b%d g%d %c %lld\n", blockIdx.x, threadIdx.x / 128, tr_c[threadIdx.x / 128][i],
+             tr_t[threadIdx.x / 128][i] - tr_t[threadIdx.x / 128][0]);
+#endif
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
