@@ -1031,6 +1031,141 @@ k_bsgs_ext(BsgsExtArgs A, LfDev dv) {
 }
 
 // ---------------------------------------------------------------------------------------
+// k_bsgs_ext for beta = BETA known at compile time, software-pipelined in registers: the
+// operands of baby rotation r + 1 (BETA pieces, 2 BETA key rows, ct.b, G diagonals: 16 B each
+// per thread) are loaded while rotation r is multiplied, permuted and accumulated, so every
+// thread keeps a whole rotation of loads (~240 B) in flight instead of one digit (48 B).
+// Same arithmetic as k_bsgs_ext, bit for bit.
+template <int BETA, int G>
+struct BsOps {
+  uint4 pc[BETA], kb[BETA], ka[BETA], b, d[G];
+};
+
+template <int L1, int L2, int G, int BETA>
+__global__ void __launch_bounds__(BsgsShape<L1, L2>::THREADS, 2)
+k_bsgs_pipe(BsgsExtArgs A, LfDev dv) {
+  using S = BsgsShape<L1, L2>;
+  constexpr int logN = L1 + L2;
+  constexpr int M2 = S::M2;
+  __shared__ u32 buf[S::LINES * M2];
+  const int ln = threadIdx.x / S::TPL, tid = threadIdx.x % S::TPL;
+  constexpr int CPR = (1 << L1) / S::LINES;
+  const int t = blockIdx.x / CPR;
+  const int hi = (blockIdx.x % CPR) * S::LINES + ln;
+  const int l = A.level;
+  const bool is_main = t <= l;
+  const int pi = is_main ? t : A.L + 1 + (t - l - 1);
+  const PrimeK pk = dv.pk[pi];
+  const int ext = A.ext;
+  u32* lb = buf + ln * M2;
+  const int e0 = tid * 4;
+  u32 pm = 0, pmp = 0;
+  if (is_main) { pm = A.pmod[2 * t]; pmp = A.pmod[2 * t + 1]; }
+  const size_t dst = ((size_t)t << logN) + ((size_t)hi << L2) + e0;
+  auto load = [&](int r, BsOps<BETA, G>& o) {
+    const int hs = (int)(auto_src_index((u32)hi << L2, A.gs[r], logN) >> L2);
+    const size_t src = ((size_t)hs << L2) + e0;
+    const u32* key = A.keyp[r];
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      o.pc[j] = __ldg(reinterpret_cast<const uint4*>(A.T1 + ((size_t)(j * ext + t) << logN) + src));
+      o.kb[j] = __ldg(reinterpret_cast<const uint4*>(key + (((size_t)(j * 2 + 0) * A.R + pi) << logN) + src));
+      o.ka[j] = __ldg(reinterpret_cast<const uint4*>(key + (((size_t)(j * 2 + 1) * A.R + pi) << logN) + src));
+    }
+    o.b = is_main ? __ldg(reinterpret_cast<const uint4*>(A.ct + ((size_t)t << logN) + src)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const u32* p = k < A.ngiant ? A.pt[k][1 + r] : nullptr;
+      o.d[k] = p ? __ldg(reinterpret_cast<const uint4*>(p + dst)) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  lf_pdl_trigger();
+  lf_pdl_wait();
+  BsOps<BETA, G> cur;
+  if (A.nrot > 0) load(0, cur);
+
+  u32 ob[G][4], oa[G][4];
+#pragma unroll
+  for (int k = 0; k < G; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { ob[k][e] = 0; oa[k][e] = 0; }
+  if (is_main) {            // identity baby: P * ct on the main rows (its special rows are zero)
+    const uint4 vb = *reinterpret_cast<const uint4*>(A.ct + dst);
+    const uint4 va = *reinterpret_cast<const uint4*>(A.ct + ((size_t)(l + 1 + t) << logN) + ((size_t)hi << L2) + e0);
+    const u32 xb[4] = {vb.x, vb.y, vb.z, vb.w}, xa[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const u32* p = A.pt[k][0];
+      if (!p) continue;
+      const uint4 pv = *reinterpret_cast<const uint4*>(p + dst);
+      const u32 pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const u32 w = mul_shoup(pw[e], pm, pmp, pk.q);
+        ob[k][e] = addmod(ob[k][e], mulmod(xb[e], w, pk), pk.q);
+        oa[k][e] = addmod(oa[k][e], mulmod(xa[e], w, pk), pk.q);
+      }
+    }
+  }
+
+#pragma unroll 1
+  for (int r = 0; r < A.nrot; ++r) {
+    BsOps<BETA, G> nxt;
+    if (r + 1 < A.nrot) load(r + 1, nxt);
+    const u32 g = A.gs[r];
+    u64 ab[4] = {0, 0, 0, 0}, aa[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      const uint4 pc = cur.pc[j], kb = cur.kb[j], ka = cur.ka[j];
+      ab[0] += (u64)pc.x * kb.x; ab[1] += (u64)pc.y * kb.y; ab[2] += (u64)pc.z * kb.z; ab[3] += (u64)pc.w * kb.w;
+      aa[0] += (u64)pc.x * ka.x; aa[1] += (u64)pc.y * ka.y; aa[2] += (u64)pc.z * ka.z; aa[3] += (u64)pc.w * ka.w;
+    }
+    u32 rb[4], ra[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { rb[e] = reduce64(ab[e], pk); ra[e] = reduce64(aa[e], pk); }
+    if (is_main) {          // + P * b, then sigma_r (source frame -> output line)
+      const u32 bw[4] = {cur.b.x, cur.b.y, cur.b.z, cur.b.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rb[e] = addmod(rb[e], mul_shoup(bw[e], pm, pmp, pk.q), pk.q);
+    }
+    u32 sl[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sl[e] = auto_src_slot_brev(((u32)hi << L2) + e0 + e, g, logN, L2);
+    __syncthreads();                       // previous rotation's reads of buf are done
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lb[brev_bits(e0 + e, L2)] = rb[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) rb[e] = lb[sl[e]];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lb[brev_bits(e0 + e, L2)] = ra[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ra[e] = lb[sl[e]];
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      if (k >= A.ngiant || !A.pt[k][1 + r]) continue;
+      const u32 pw[4] = {cur.d[k].x, cur.d[k].y, cur.d[k].z, cur.d[k].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ob[k][e] = addmod(ob[k][e], mulmod(rb[e], pw[e], pk), pk.q);
+        oa[k][e] = addmod(oa[k][e], mulmod(ra[e], pw[e], pk), pk.q);
+      }
+    }
+    cur = nxt;
+  }
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    if (k >= A.ngiant) break;
+    u32* ob_ = A.out + ((size_t)((k * 2 + 0) * ext + t) << logN) + ((size_t)hi << L2) + e0;
+    u32* oa_ = A.out + ((size_t)((k * 2 + 1) * ext + t) << logN) + ((size_t)hi << L2) + e0;
+    *reinterpret_cast<uint4*>(ob_) = make_uint4(ob[k][0], ob[k][1], ob[k][2], ob[k][3]);
+    *reinterpret_cast<uint4*>(oa_) = make_uint4(oa[k][0], oa[k][1], oa[k][2], oa[k][3]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // K_E: row pass of the NTT of the converted rows, (acc - conv) * scalar, epilogue.
 enum { EPI_KS = 0, EPI_MUL = 1, EPI_ROT = 2 };
 struct ModDownArgs {
@@ -1408,6 +1543,18 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.T1 = w.T1; A.pmod = P->pmod; A.level = c.level; A.L = P->L; A.alpha = alpha;
     A.beta = K.beta; A.R = P->L + 1 + alpha; A.ext = K.ext;
     dim3 grid(K.ext * ((1 << L1) / SB::LINES));
+    static int pipe = -1;
+    if (pipe < 0) pipe = env_int("LF_BSGS_PIPE", 1);
+    if (pipe && A.beta == 4) {
+      switch (A.ngiant) {
+#define LF_BP(GG) case GG: LF_LAUNCH_CHECK(lf_launch(k_bsgs_pipe<L1, L2, GG, 4>, grid, dim3(SB::THREADS), 0, s, 1, A, dv)); break;
+        LF_BP(1) LF_BP(2) LF_BP(3) LF_BP(4)
+#undef LF_BP
+        default: lf_set_error("bsgs: %d giant steps (max %d)", A.ngiant, LF_BSGS_GMAX); return 2;
+      }
+      LF_CHECK_LAUNCH();
+      return 0;
+    }
     switch (A.ngiant) {
 #define LF_BG(GG) case GG: LF_LAUNCH_CHECK(lf_launch(k_bsgs_ext<L1, L2, GG>, grid, dim3(SB::THREADS), 0, s, 1, A, dv)); break;
       LF_BG(1) LF_BG(2) LF_BG(3) LF_BG(4)
