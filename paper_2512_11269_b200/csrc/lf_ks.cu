@@ -1036,13 +1036,16 @@ k_bsgs_ext(BsgsExtArgs A, LfDev dv) {
 // per thread) are loaded while rotation r is multiplied, permuted and accumulated, so every
 // thread keeps a whole rotation of loads (~240 B) in flight instead of one digit (48 B).
 // Same arithmetic as k_bsgs_ext, bit for bit.
+#ifndef LF_BSGS_MINB
+#define LF_BSGS_MINB 2
+#endif
 template <int BETA, int G>
 struct BsOps {
   uint4 pc[BETA], kb[BETA], ka[BETA], b, d[G];
 };
 
 template <int L1, int L2, int G, int BETA>
-__global__ void __launch_bounds__(BsgsShape<L1, L2>::THREADS, 2)
+__global__ void __launch_bounds__(BsgsShape<L1, L2>::THREADS, LF_BSGS_MINB)
 k_bsgs_pipe(BsgsExtArgs A, LfDev dv) {
   using S = BsgsShape<L1, L2>;
   constexpr int logN = L1 + L2;
@@ -1110,8 +1113,6 @@ k_bsgs_pipe(BsgsExtArgs A, LfDev dv) {
 
 #pragma unroll 1
   for (int r = 0; r < A.nrot; ++r) {
-    BsOps<BETA, G> nxt;
-    if (r + 1 < A.nrot) load(r + 1, nxt);
     const u32 g = A.gs[r];
     u64 ab[4] = {0, 0, 0, 0}, aa[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -1120,11 +1121,20 @@ k_bsgs_pipe(BsgsExtArgs A, LfDev dv) {
       ab[0] += (u64)pc.x * kb.x; ab[1] += (u64)pc.y * kb.y; ab[2] += (u64)pc.z * kb.z; ab[3] += (u64)pc.w * kb.w;
       aa[0] += (u64)pc.x * ka.x; aa[1] += (u64)pc.y * ka.y; aa[2] += (u64)pc.z * ka.z; aa[3] += (u64)pc.w * ka.w;
     }
+    // rotation r + 1's operands are requested once this rotation's pieces and keys are
+    // consumed (their registers are free), and land during the reduction, sigma and the
+    // diagonal MACs below
+    BsOps<BETA, G> nxt;
+    const uint4 bcur = cur.b;
+    uint4 dcur[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) dcur[k] = cur.d[k];
+    if (r + 1 < A.nrot) load(r + 1, nxt);
     u32 rb[4], ra[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) { rb[e] = reduce64(ab[e], pk); ra[e] = reduce64(aa[e], pk); }
     if (is_main) {          // + P * b, then sigma_r (source frame -> output line)
-      const u32 bw[4] = {cur.b.x, cur.b.y, cur.b.z, cur.b.w};
+      const u32 bw[4] = {bcur.x, bcur.y, bcur.z, bcur.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) rb[e] = addmod(rb[e], mul_shoup(bw[e], pm, pmp, pk.q), pk.q);
     }
@@ -1146,7 +1156,7 @@ k_bsgs_pipe(BsgsExtArgs A, LfDev dv) {
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       if (k >= A.ngiant || !A.pt[k][1 + r]) continue;
-      const u32 pw[4] = {cur.d[k].x, cur.d[k].y, cur.d[k].z, cur.d[k].w};
+      const u32 pw[4] = {dcur[k].x, dcur[k].y, dcur[k].z, dcur[k].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         ob[k][e] = addmod(ob[k][e], mulmod(rb[e], pw[e], pk), pk.q);
