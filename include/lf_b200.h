@@ -130,6 +130,13 @@ int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* 
                        const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
                        size_t out_bstride, int batch, void* workspace, void* stream);
 
+/* lf_hom_mul_rescale over ciphertexts whose polynomials are ct_pitch >= level + 1 rows apart
+ * (the a rows of instance i start at ct1 + i * ct_bstride + ct_pitch * N): a level-dropped
+ * row-prefix view of a higher-level ciphertext block is used in place, without a copy. */
+int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
+                         const uint32_t* ct2, size_t ct_bstride, int ct_pitch, const uint32_t* rlk,
+                         uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
+
 /* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
  * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a
  * rotation, 2N-1 for conjugation. */
@@ -216,6 +223,12 @@ int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstri
 int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct,
                      size_t ct_bstride, uint32_t* out, size_t out_bstride, int batch,
                      void* workspace, void* stream);
+
+/* lf_rescale_multi over ciphertexts whose polynomials are ct_pitch >= level + 1 rows apart
+ * (row-prefix views of higher-level blocks, as lf_hom_mul_rescale_p). */
+int lf_rescale_multi_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct, size_t ct_bstride,
+                       int ct_pitch, uint32_t* out, size_t out_bstride, int batch, void* workspace,
+                       void* stream);
 
 /* keyswitch_decompose (ckks.py:95-117) materialised: pieces = beta x (level+1+alpha) rows,
  * eval domain, digit-major; beta = min(d, level+1).  Workspace as lf_keyswitch (batch 1). */

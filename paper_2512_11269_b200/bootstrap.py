@@ -306,6 +306,14 @@ def evalmod_plain(x: np.ndarray, cfg: BootConfig) -> np.ndarray:
 # the algorithm over a backend
 # ---------------------------------------------------------------------------------------
 
+class _ChebPowers(dict):
+    """T_k by k, plus the odd powers stored as T_k + T_1 (`folded`)."""
+
+    def __init__(self, *a):
+        super().__init__(*a)
+        self.folded = set()
+
+
 class CkksCircuit:
     """Scale / level bookkeeping and the homomorphic building blocks shared by the bootstrap
     and the encrypted layer workloads (workloads.py): BSGS linear maps with hoisted rotations
@@ -405,11 +413,21 @@ class CkksCircuit:
         return be.rescale2(be.hom_mul(a, b))
 
     def _cheb_powers(self, u, degree=None):
-        """T_1..T_(baby-1) and the giant powers T_baby, T_2baby, ... up to `degree`."""
+        """T_1..T_(baby-1) and the giant powers T_baby, T_2baby, ... up to `degree`.
+
+        T_3 = T_1 (2 T_2 - 1) (one product, no subtraction).  An odd power T_2k+1 (k >= 2)
+        that no later product reads is kept as 2 T_k T_k+1 = T_2k+1 + T_1: its -T_1 moves into
+        the T_1 coefficient of the leaf combinations (`_leaf`), which saves the exact scale
+        match of T_1 (a constant product and a double rescale) per such power."""
         be = self.be
-        T = {1: u}
+        T = _ChebPowers({1: u})
         g = self.cfg.baby
         degree = self.cfg.cheb_degree if degree is None else degree
+        read = {m // 2 for m in range(2, g)} | {m // 2 + 1 for m in range(3, g, 2)}
+        G = g
+        while G <= degree:
+            read.add(G // 2)
+            G *= 2
 
         def twice(x):
             # 2x: the same residues at half the declared scale (free) while the scale stays
@@ -424,7 +442,12 @@ class CkksCircuit:
             return be.add_const(x, -1.0)
 
         def odd(k):                             # T_2k+1 = 2 T_k T_k+1 - T_1
+            if k == 1:                          # T_3 = T_1 (2 T_2 - 1)
+                return self._mul2(T[1], be.add_const(twice(T[2]), -1.0))
             x = twice(self._mul2(T[k], T[k + 1]))
+            if 2 * k + 1 not in read:
+                T.folded.add(2 * k + 1)
+                return x
             return be.sub(x, self._match(T[1], x.level, x.scale))
 
         for m in range(2, g):
@@ -438,8 +461,13 @@ class CkksCircuit:
     def _leaf(self, c, T, level, scale):
         """sum_i c_i T_i (i < baby) at exactly (level, scale): every term is dropped to
         level + 2 and multiplied by c_i encoded at the scale that makes all products share
-        scale * q_{level+2} q_{level+1}; one linear combination, one double rescale."""
+        scale * q_{level+2} q_{level+1}; one linear combination, one double rescale.  Powers
+        stored as T_m + T_1 (`_cheb_powers`) take their -T_1 through the T_1 coefficient."""
         be = self.be
+        c = np.array(c, dtype=np.float64)
+        for m in getattr(T, "folded", ()):
+            if m < len(c) and c[m] != 0.0:
+                c[1] -= c[m]
         terms = []
         for i in range(1, len(c)):
             if c[i] == 0.0:
@@ -643,6 +671,16 @@ class CtBatch:
 
     def dense(self):
         return self if self.data.is_contiguous() else CtBatch(self.data.contiguous(), self.scale, self.level)
+
+    def pitched(self):
+        """(instance stride, rows per polynomial) when `data` is a row-prefix view of a
+        contiguous (B, 2, P, N) block (the pitched kernels take it in place), else None."""
+        d = self.data
+        N = d.shape[-1]
+        st = d.stride()
+        if st[3] == 1 and st[2] == N and st[1] % N == 0 and st[0] == 2 * st[1]:
+            return st[0], st[1] // N
+        return None
 
 
 def map_batch(fn, *args):
@@ -992,13 +1030,16 @@ class GpuBackend:
             from . import _native
             from .context import dptr, get_context, stream_handle
             ctx = get_context(self.params)
-            x = x.dense()
+            pv = x.pitched()
+            if pv is None:
+                x = x.dense()
+                pv = (x.data[0].numel(), x.level + 1)
             B = x.data.shape[0]
             ws = ctx.rescale_workspace(x.level, B)
             out = torch.empty((B, 2, x.level - 1, self.params.N), dtype=torch.int32, device=x.data.device)
-            _native.check(_native.lib().lf_rescale_multi(ctx.handle, x.level, 2, dptr(x.data), x.data[0].numel(),
-                                                         dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
-                          "lf_rescale_multi")
+            _native.check(_native.lib().lf_rescale_multi_p(ctx.handle, x.level, 2, dptr(x.data, strided=True), pv[0],
+                                                           pv[1], dptr(out), out[0].numel(), B, dptr(ws),
+                                                           stream_handle()), "lf_rescale_multi_p")
             return CtBatch(out, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
         b, a = fused.rescale_multi(self.params, x, 2)
         q = self.params.rns_basis
@@ -1014,20 +1055,25 @@ class GpuBackend:
         scale = x.scale * y.scale / q[x.level] / q[x.level - 1]
         ctx = get_context(self.params)
         if isinstance(x, CtBatch):
-            x, y = x.dense(), y.dense()
             assert x.data.shape == y.data.shape
+            px, py = x.pitched(), y.pitched()
+            if px is None or px != py:
+                x, y = x.dense(), y.dense()
+                px = (x.data[0].numel(), x.level + 1)
             B = x.data.shape[0]
             c1, c2 = x.data, y.data
+            bs, pitch = px
         else:
             from .fused import ct_block
             B = 1
             c1, c2 = ct_block(x), ct_block(y)
+            bs, pitch = c1.numel(), x.level + 1
         ws = ctx.ks_workspace(x.level, B)
         out = torch.empty((B, 2, x.level - 1, self.N), dtype=torch.int32, device=c1.device)
-        _native.check(_native.lib().lf_hom_mul_rescale(ctx.handle, x.level, 2, dptr(c1), dptr(c2),
-                                                       c1.numel() // B, dptr(self.rlk.data), dptr(out),
-                                                       out[0].numel(), B, dptr(ws), stream_handle()),
-                      "lf_hom_mul_rescale")
+        _native.check(_native.lib().lf_hom_mul_rescale_p(ctx.handle, x.level, 2, dptr(c1, strided=True),
+                                                         dptr(c2, strided=True), bs, pitch, dptr(self.rlk.data),
+                                                         dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
+                      "lf_hom_mul_rescale_p")
         if isinstance(x, CtBatch):
             return CtBatch(out, scale, x.level - 2)
         from .poly import Domain, RnsPolynomial, main_ids

@@ -32,12 +32,17 @@ def stream_handle():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def dptr(t: torch.Tensor):
+def dptr(t: torch.Tensor, strided: bool = False):
     """Raw device pointer for the C ABI: the kernels index rows densely, so a strided view or
-    a tensor on another GPU than the current one is rejected instead of read out of bounds."""
+    a tensor on another GPU than the current one is rejected instead of read out of bounds.
+    `strided=True` (the pitched entry points, which take the strides explicitly) only requires
+    whole contiguous rows."""
     if not t.is_cuda:
         raise _native.NativeError("expected a CUDA tensor")
-    if not t.is_contiguous():
+    if strided:
+        if t.stride(-1) != 1 or (t.dim() > 1 and t.stride(-2) != t.shape[-1]):
+            raise _native.NativeError(f"expected contiguous rows (strides {t.stride()})")
+    elif not t.is_contiguous():
         raise _native.NativeError(f"expected a contiguous tensor (shape {tuple(t.shape)}, strides {t.stride()})")
     if t.device.index != torch.cuda.current_device():
         raise _native.NativeError(f"tensor on cuda:{t.device.index}, current device cuda:{torch.cuda.current_device()}")

@@ -1486,6 +1486,7 @@ struct KsCall {
   int rescale_nd;           // MUL: fuse a rescale by this many primes into the ModDown (0: none)
   bool kperm;               // ROT: keys in permuted form (lf_permute_rotation_key)
   const BsgsExtArgs* bsgs;  // hoisted ROT: K_C fused with the giant-step sums (k_bsgs_ext)
+  int pitch;                // MUL: rows per polynomial of ct1 / ct2 (>= level + 1; 0: level + 1)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -1584,7 +1585,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.ext_out = c.ext_out ? 1 : 0;
     A.pre = pre ? 1 : 0;
     A.fuse_nd = nd; A.t2_rows = alpha + nd;
-    A.c1 = c.e0; A.c2 = c.e1; A.c_bs = c.e_bs; A.c_ne = l1;
+    A.c1 = c.e0; A.c2 = c.e1; A.c_bs = c.e_bs; A.c_ne = c.pitch > 0 ? c.pitch : l1;
     A.pmod = P->pmod;
     if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
@@ -1624,7 +1625,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     ModDownArgs A{};
     A.T3 = w.T3; A.acc = w.acc; A.out = c.out; A.e0 = c.e0; A.e1 = c.e1;
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
-    A.scal = P->rowk + 2; A.sstride = 4; A.nt = nt; A.nacc = l1; A.ne = l1;
+    A.scal = P->rowk + 2; A.sstride = 4; A.nt = nt; A.nacc = l1; A.ne = c.pitch > 0 ? c.pitch : l1;
     if (nd) {
       A.scal = P->pqinv[nd - 1] + (size_t)c.level * P->n_main * 2; A.sstride = 2;
       A.dscal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)c.level * P->n_main * 2;
@@ -1649,7 +1650,8 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
 // floor(floor(X/a)/b) = floor(X/(ab)) for the exact representative X >= 0).
 template <int L1, int L2>
 static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, size_t ct_bs,
-                            u32* out, size_t out_bs, int batch, void* ws, cudaStream_t s) {
+                            u32* out, size_t out_bs, int batch, void* ws, cudaStream_t s, int pitch = 0) {
+  if (pitch <= 0) pitch = level + 1;           // rows per polynomial of ct
   using S = NttShape<L1, L2>;
   const LfKsPlan* P = ctx->ks;
   const KsLevelPlan& K = P->lv[level];
@@ -1664,7 +1666,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, l + 1, nt, nt, batch, 1, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, pitch, nt, nt, batch, 1, 1)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1681,7 +1683,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
     A.T3 = T3; A.acc = ct; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
     A.t3_bs = per; A.acc_bs = ct_bs; A.out_bs = out_bs; A.e_bs = 0;
     A.scal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)l * P->n_main * 2; A.sstride = 2;
-    A.nt = nt; A.nacc = l + 1; A.ne = 0;
+    A.nt = nt; A.nacc = pitch; A.ne = 0;
     A.nbatch = batch;
     A.bpc = 1;
     dim3 grid(nt * groups, 1, batch);
@@ -1862,15 +1864,23 @@ int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t
 int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
                        const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
                        size_t out_bstride, int batch, void* workspace, void* stream) {
+  return lf_hom_mul_rescale_p(ctx, level, ndrop, ct1, ct2, ct_bstride, level + 1, rlk, out, out_bstride,
+                              batch, workspace, stream);
+}
+
+int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
+                         const uint32_t* ct2, size_t ct_bstride, int ct_pitch, const uint32_t* rlk,
+                         uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
   if (int e = ks_check(ctx, level)) return e;
   if (!ct1 || !ct2 || !rlk || !out || !workspace) { lf_set_error("lf_hom_mul_rescale: null argument"); return 1; }
   if (ndrop < 1 || ndrop > 2 || level < ndrop) {
     lf_set_error("lf_hom_mul_rescale: cannot drop %d primes at level %d", ndrop, level);
     return 2;
   }
-  const size_t arow = (size_t)(level + 1) * ctx->N;
+  if (ct_pitch < level + 1) { lf_set_error("lf_hom_mul_rescale_p: row pitch %d < level + 1", ct_pitch); return 2; }
+  const size_t arow = (size_t)ct_pitch * ctx->N;
   KsCall c{};
-  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop;
+  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop; c.pitch = ct_pitch;
   c.x = ct1 + arow; c.x2 = ct2 + arow; c.x_bs = ct_bstride; c.key = rlk; c.key_bs = 0;
   c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct_bstride;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
@@ -1989,11 +1999,17 @@ int lf_rescale(const lf_ctx* ctx, int level, const uint32_t* ct, size_t ct_bstri
 
 int lf_rescale_multi(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct, size_t ct_bstride,
                      uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+  return lf_rescale_multi_p(ctx, level, ndrop, ct, ct_bstride, level + 1, out, out_bstride, batch, workspace, stream);
+}
+
+int lf_rescale_multi_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct, size_t ct_bstride, int ct_pitch,
+                       uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
   if (int e = ks_check(ctx, level)) return e;
+  if (ct_pitch < level + 1) { lf_set_error("lf_rescale_multi_p: row pitch %d < level + 1", ct_pitch); return 2; }
   if (ndrop < 1 || ndrop > 2) { lf_set_error("lf_rescale_multi: ndrop %d not in {1, 2}", ndrop); return 2; }
   if (level < ndrop) { lf_set_error("rescale by %d primes at level %d", ndrop, level); return 2; }
   if (!ct || !out || !workspace) { lf_set_error("lf_rescale_multi: null argument"); return 1; }
-#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ndrop, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+#define LF_RS(A, B) { if (int e = rescale_pipeline<A, B>(ctx, level, ndrop, ct, ct_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream, ct_pitch)) return e; }
   LF_DISPATCH_LOGN(ctx->logN, LF_RS)
 #undef LF_RS
   return 0;

@@ -148,3 +148,27 @@ def test_ptmac_and_lincomb_equal_unfused(env):
         acc = m if acc is None else B.hom_add(acc, m, p)
     assert lc.scale == acc.scale
     assert torch.equal(lc.b.limbs, acc.b.limbs) and torch.equal(lc.a.limbs, acc.a.limbs)
+
+
+def test_pitched_views_equal_dense(env):
+    """lf_hom_mul_rescale_p / lf_rescale_multi_p on level-dropped row-prefix views of a batch
+    (no copy) give the residues of the same calls on contiguous copies."""
+    import torch
+    B, O, p, P, sk, rlk, ko, rk, rko, steps, ct, cto = env
+    from paper_2512_11269_b200 import bootstrap as BT
+    be = BT.GpuBackend(p, rlk, None, rk)
+    ct2 = B.encrypt(B.encode(np.random.default_rng(3).uniform(-1, 1, p.n), p), B.keygen(p, seed=11)[1], p,
+                    np.random.default_rng(4))
+    x = be.stack([ct, ct2])
+    y = be.stack([ct2, ct])
+    lv = p.max_level - 2
+    xv, yv = be.drop_to_level(x, lv), be.drop_to_level(y, lv)
+    assert not xv.data.is_contiguous() and xv.pitched() is not None
+    xd, yd = BT.CtBatch(xv.data.contiguous(), xv.scale, lv), BT.CtBatch(yv.data.contiguous(), yv.scale, lv)
+    got, want = be.mul_rescale2(xv, yv), be.mul_rescale2(xd, yd)
+    assert torch.equal(got.data, want.data) and got.level == want.level == lv - 2
+    got, want = be.rescale2(xv), be.rescale2(xd)
+    assert torch.equal(got.data, want.data)
+    # a batch of single ciphertexts through the same pitched entry point equals the unbatched op
+    one = be.mul_rescale2(be.drop_to_level(ct, lv), be.drop_to_level(ct2, lv))
+    assert np.array_equal(one.b.numpy(), be.mul_rescale2(xd, yd).data[0, 0].cpu().numpy())
