@@ -130,12 +130,14 @@ int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* 
                        const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
                        size_t out_bstride, int batch, void* workspace, void* stream);
 
-/* lf_hom_mul_rescale over ciphertexts whose polynomials are ct_pitch >= level + 1 rows apart
- * (the a rows of instance i start at ct1 + i * ct_bstride + ct_pitch * N): a level-dropped
- * row-prefix view of a higher-level ciphertext block is used in place, without a copy. */
+/* lf_hom_mul_rescale over ciphertexts whose polynomials are ct*_pitch >= level + 1 rows apart
+ * (the a rows of instance i of ct1 start at ct1 + i * ct1_bstride + ct1_pitch * N; ct2 has its
+ * own stride and pitch): level-dropped row-prefix views of higher-level ciphertext blocks are
+ * used in place, without a copy. */
 int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
-                         const uint32_t* ct2, size_t ct_bstride, int ct_pitch, const uint32_t* rlk,
-                         uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
+                         size_t ct1_bstride, int ct1_pitch, const uint32_t* ct2, size_t ct2_bstride,
+                         int ct2_pitch, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
+                         int batch, void* workspace, void* stream);
 
 /* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
  * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a

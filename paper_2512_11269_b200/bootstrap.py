@@ -998,10 +998,17 @@ class GpuBackend:
         import torch
         from .poly import ewise
         assert x.level == y.level and x.scale == y.scale and x.data.shape == y.data.shape
-        x, y = x.dense(), y.dense()
-        out = torch.empty_like(x.data)
-        n = x.data.shape[0] * 2 * (x.level + 1)
-        ewise(self.params, op, out.view(n, -1), x.data.view(n, -1), self._rows_pidx(x), b=y.data.view(n, -1))
+        out = torch.empty(x.data.shape, dtype=x.data.dtype, device=x.data.device)
+        if x.data.is_contiguous() and y.data.is_contiguous():
+            n = x.data.shape[0] * 2 * (x.level + 1)
+            ewise(self.params, op, out.view(n, -1), x.data.view(n, -1), self._rows_pidx(x), b=y.data.view(n, -1))
+        else:
+            # level-dropped views: one launch per polynomial (its rows are contiguous) instead
+            # of a copy of the whole batch
+            ids = tuple(range(x.level + 1))
+            for i in range(x.data.shape[0]):
+                for k in range(2):
+                    ewise(self.params, op, out[i, k], x.data[i, k], ids, b=y.data[i, k])
         return CtBatch(out, x.scale, x.level)
 
     def add(self, x, y):
@@ -1057,21 +1064,23 @@ class GpuBackend:
         if isinstance(x, CtBatch):
             assert x.data.shape == y.data.shape
             px, py = x.pitched(), y.pitched()
-            if px is None or px != py:
-                x, y = x.dense(), y.dense()
+            if px is None:
+                x = x.dense()
                 px = (x.data[0].numel(), x.level + 1)
+            if py is None:
+                y = y.dense()
+                py = (y.data[0].numel(), y.level + 1)
             B = x.data.shape[0]
             c1, c2 = x.data, y.data
-            bs, pitch = px
         else:
             from .fused import ct_block
             B = 1
             c1, c2 = ct_block(x), ct_block(y)
-            bs, pitch = c1.numel(), x.level + 1
+            px, py = (c1.numel(), x.level + 1), (c2.numel(), y.level + 1)
         ws = ctx.ks_workspace(x.level, B)
         out = torch.empty((B, 2, x.level - 1, self.N), dtype=torch.int32, device=c1.device)
-        _native.check(_native.lib().lf_hom_mul_rescale_p(ctx.handle, x.level, 2, dptr(c1, strided=True),
-                                                         dptr(c2, strided=True), bs, pitch, dptr(self.rlk.data),
+        _native.check(_native.lib().lf_hom_mul_rescale_p(ctx.handle, x.level, 2, dptr(c1, strided=True), px[0], px[1],
+                                                         dptr(c2, strided=True), py[0], py[1], dptr(self.rlk.data),
                                                          dptr(out), out[0].numel(), B, dptr(ws), stream_handle()),
                       "lf_hom_mul_rescale_p")
         if isinstance(x, CtBatch):
@@ -1264,13 +1273,20 @@ class GpuBackend:
         k = round(Fraction(c) * Fraction(ct.scale))
         ids = main_ids(ct.level)
         if isinstance(ct, CtBatch):
-            ct = ct.dense()
             B = ct.data.shape[0]
-            n = B * 2 * (ct.level + 1)
-            sc = (self._scalar_rows(ct, k) + [0] * (ct.level + 1)) * B       # b rows only
-            out = torch.empty_like(ct.data)
-            ewise(self.params, LF_OP_ADD_SCALAR, out.view(n, -1), ct.data.view(n, -1), self._rows_pidx(ct),
-                  scalars=sc)
+            out = torch.empty(ct.data.shape, dtype=ct.data.dtype, device=ct.data.device)
+            if ct.data.is_contiguous():
+                n = B * 2 * (ct.level + 1)
+                sc = (self._scalar_rows(ct, k) + [0] * (ct.level + 1)) * B       # b rows only
+                ewise(self.params, LF_OP_ADD_SCALAR, out.view(n, -1), ct.data.view(n, -1), self._rows_pidx(ct),
+                      scalars=sc)
+            else:                              # a level-dropped view: per polynomial, no copy
+                rows = tuple(range(ct.level + 1))
+                for i in range(B):
+                    ewise(self.params, LF_OP_ADD_SCALAR, out[i, 0], ct.data[i, 0], rows,
+                          scalars=self._scalar_rows(ct, k))
+                    ewise(self.params, LF_OP_ADD_SCALAR, out[i, 1], ct.data[i, 1], rows,
+                          scalars=[0] * len(rows))
             return CtBatch(out, ct.scale, ct.level)
         out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
         ewise(self.params, LF_OP_ADD_SCALAR, out[0], ct.b.limbs, ids, scalars=self._scalar_rows(ct, k))

@@ -61,7 +61,7 @@ template <int L1, int L2, int MODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
            size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase,
-           int nbatch, int bpc, int pstep) {
+           int nbatch, int bpc, int pstep, size_t x2_bs, int src_rs2) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int GROUPS = (1 << L1) / S::LPCR;
@@ -86,7 +86,7 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
     load_row_step2<L2>(v, x + off, tl);
     if (MODE == 1) {
       u32 w[C::E];
-      load_row_step2<L2>(w, x2 + off, tl);
+      load_row_step2<L2>(w, x2 + (size_t)b * x2_bs + (((size_t)((row / rpp) * src_rs2 + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2)), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
     }
@@ -642,8 +642,9 @@ struct KsInnerArgs {
                        // rows get + P*(d0, d1) and join the special rows in T2 (t2_rows per poly)
   int t2_rows;
   const u32 *c1, *c2;  // fuse_nd: ct1, ct2 (b rows then a rows, c_ne rows per poly)
-  size_t c_bs;
-  int c_ne;
+  size_t c_bs, c2_bs;  // instance strides of ct1 / ct2
+  int c_ne, c2_ne;     // rows per polynomial of ct1 / ct2
+  size_t x2_bs;        // instance stride of x2
   const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
   u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
   // limb-sharded pipeline (null tmap: one device holds every row): CTA row r of this rank's
@@ -763,7 +764,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
           }
         }
       } else {
-        const u32* xr2 = A.x2 + b * A.x_bs + ((size_t)r << logN);
+        const u32* xr2 = A.x2 + b * A.x2_bs + ((size_t)r << logN);
         load_row_step2<L2>(pc, xr + ((size_t)hi << L2), tl);
         if (XMODE == 1) {
           u32 w[C::E];
@@ -858,7 +859,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
       // + P * (d0, d1) (ckks.py:189-193: d0 = b1 b2, d1 = b1 a2 + a1 b2) before the division
       const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
       const u32* c1 = A.c1 + b * A.c_bs;
-      const u32* c2 = A.c2 + b * A.c_bs;
+      const u32* c2 = A.c2 + b * A.c2_bs;
       const size_t lo = (size_t)hi << L2;
       u32 b1[C::E], b2[C::E], o[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo, tl);
@@ -866,7 +867,7 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e)
         rb[e] = addmod(rb[e], mul_shoup(mulmod(b1[e], b2[e], pk), pm, pmp, pk.q), pk.q);
-      load_row_step2<L2>(o, c2 + ((size_t)(A.c_ne + t) << logN) + lo, tl);      // a2
+      load_row_step2<L2>(o, c2 + ((size_t)(A.c2_ne + t) << logN) + lo, tl);     // a2
 #pragma unroll
       for (int e = 0; e < C::E; ++e) b1[e] = mulmod(b1[e], o[e], pk);          // b1 a2
       load_row_step2<L2>(o, c1 + ((size_t)(A.c_ne + t) << logN) + lo, tl);      // a1
@@ -1184,11 +1185,12 @@ struct ModDownArgs {
   u32* out;            // 2 x nt rows
   const u32* e0;       // epilogue inputs (ct1 for MUL: b1 | a1 ; ct for ROT)
   const u32* e1;       // ct2 for MUL
-  size_t t3_bs, acc_bs, out_bs, e_bs;
+  size_t t3_bs, acc_bs, out_bs, e_bs, e1_bs;
   const u32* scal;     // per target t: scalar, Shoup companion at scal[t*sstride], +1
   int sstride;
   const u32* dscal;    // EPI_MUL fused with a rescale: (q_l [q_{l-1}])^-1 for the d terms, stride 2
   int nt, nacc, ne;    // targets, acc rows per poly, epilogue rows per poly
+  int ne1;             // rows per poly of e1 (EPI_MUL)
   int nbatch, bpc;     // instances; instances per CTA (sharing the staged twiddles)
   u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
   const int* tmap;     // limb-sharded: storage row r is main prime tmap[r] (null: r)
@@ -1247,7 +1249,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
     if (EPI == EPI_MUL) {
       // d0 = b1*b2 ; d1 = b1*a2 + a1*b2  (ckks.py:189-193)
       const u32* c1 = A.e0 + b * A.e_bs;
-      const u32* c2 = A.e1 + b * A.e_bs;
+      const u32* c2 = A.e1 + b * A.e1_bs;
       u32 b1[C::E], b2[C::E], o1[C::E], o2[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo0, tl);
       load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo0, tl);
@@ -1261,7 +1263,7 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
         }
       } else {
         load_row_step2<L2>(o1, c1 + ((size_t)(A.ne + t) << logN) + lo0, tl);
-        load_row_step2<L2>(o2, c2 + ((size_t)(A.ne + t) << logN) + lo0, tl);
+        load_row_step2<L2>(o2, c2 + ((size_t)(A.ne1 + t) << logN) + lo0, tl);
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           u32 d1 = reduce64((u64)b1[e] * o2[e] + (u64)o1[e] * b2[e], pk);
@@ -1486,7 +1488,11 @@ struct KsCall {
   int rescale_nd;           // MUL: fuse a rescale by this many primes into the ModDown (0: none)
   bool kperm;               // ROT: keys in permuted form (lf_permute_rotation_key)
   const BsgsExtArgs* bsgs;  // hoisted ROT: K_C fused with the giant-step sums (k_bsgs_ext)
-  int pitch;                // MUL: rows per polynomial of ct1 / ct2 (>= level + 1; 0: level + 1)
+  size_t x2s() const { return sep2 ? x2_bs : x_bs; }
+  size_t e1s() const { return sep2 ? e1_bs : e_bs; }
+  int pitch, pitch2;        // MUL: rows per polynomial of ct1 / ct2 (>= level + 1; 0: level + 1)
+  size_t x2_bs, e1_bs;      // MUL: instance strides of a2 / ct2 (used when sep2)
+  bool sep2;                // ct2 has its own stride and pitch (else those of ct1)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
 };
@@ -1517,9 +1523,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     const int bpc_in = nsh >= 2 * LF_BPC ? LF_BPC : 1;      // instances per CTA (shared twiddles)
     dim3 grid(l1 * groups, 1, (nsh + bpc_in - 1) / bpc_in);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, c.x2s(), l1)); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, (size_t)0, 0)); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -1586,6 +1592,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.pre = pre ? 1 : 0;
     A.fuse_nd = nd; A.t2_rows = alpha + nd;
     A.c1 = c.e0; A.c2 = c.e1; A.c_bs = c.e_bs; A.c_ne = c.pitch > 0 ? c.pitch : l1;
+    A.c2_bs = c.e1s(); A.c2_ne = c.sep2 ? (c.pitch2 > 0 ? c.pitch2 : l1) : A.c_ne; A.x2_bs = c.x2s();
     A.pmod = P->pmod;
     if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
@@ -1624,8 +1631,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   {
     ModDownArgs A{};
     A.T3 = w.T3; A.acc = w.acc; A.out = c.out; A.e0 = c.e0; A.e1 = c.e1;
-    A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs;
+    A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs; A.e1_bs = c.e1s();
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = nt; A.nacc = l1; A.ne = c.pitch > 0 ? c.pitch : l1;
+    A.ne1 = c.sep2 ? (c.pitch2 > 0 ? c.pitch2 : l1) : A.ne;
     if (nd) {
       A.scal = P->pqinv[nd - 1] + (size_t)c.level * P->n_main * 2; A.sstride = 2;
       A.dscal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)c.level * P->n_main * 2;
@@ -1666,7 +1674,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, pitch, nt, nt, batch, 1, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, pitch, nt, nt, batch, 1, 1, (size_t)0, 0)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1710,7 +1718,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
   u32* T3 = T2 + 2 * (size_t)alpha * N;
   {
     dim3 grid(2 * alpha * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1, 1, (size_t)0, 0)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1755,7 +1763,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1, 1)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1, 1, (size_t)0, 0)); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1807,10 +1815,10 @@ static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
     KsCall k = c;
     k.batch = c.batch - b0 < LF_MAXB ? c.batch - b0 : LF_MAXB;
     k.x = c.x + (c.hoisted ? 0 : b0 * c.x_bs);
-    if (c.x2) k.x2 = c.x2 + (c.hoisted ? 0 : b0 * c.x_bs);
+    if (c.x2) k.x2 = c.x2 + (c.hoisted ? 0 : b0 * c.x2s());
     k.out = c.out + b0 * c.out_bs;
     if (c.e0) k.e0 = c.e0 + (c.hoisted ? 0 : b0 * c.e_bs);
-    if (c.e1) k.e1 = c.e1 + (c.hoisted ? 0 : b0 * c.e_bs);
+    if (c.e1) k.e1 = c.e1 + (c.hoisted ? 0 : b0 * c.e1s());
     k.b0 = b0;
     if (int e = run_ks_chunk(ctx, k, ws, s, nullptr)) return e;
   }
@@ -1864,25 +1872,30 @@ int lf_hom_mul(const lf_ctx* ctx, int level, const uint32_t* ct1, const uint32_t
 int lf_hom_mul_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
                        const uint32_t* ct2, size_t ct_bstride, const uint32_t* rlk, uint32_t* out,
                        size_t out_bstride, int batch, void* workspace, void* stream) {
-  return lf_hom_mul_rescale_p(ctx, level, ndrop, ct1, ct2, ct_bstride, level + 1, rlk, out, out_bstride,
-                              batch, workspace, stream);
+  return lf_hom_mul_rescale_p(ctx, level, ndrop, ct1, ct_bstride, level + 1, ct2, ct_bstride, level + 1, rlk,
+                              out, out_bstride, batch, workspace, stream);
 }
 
-int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1,
-                         const uint32_t* ct2, size_t ct_bstride, int ct_pitch, const uint32_t* rlk,
-                         uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t* ct1, size_t ct1_bstride,
+                         int ct1_pitch, const uint32_t* ct2, size_t ct2_bstride, int ct2_pitch,
+                         const uint32_t* rlk, uint32_t* out, size_t out_bstride, int batch, void* workspace,
+                         void* stream) {
   if (int e = ks_check(ctx, level)) return e;
   if (!ct1 || !ct2 || !rlk || !out || !workspace) { lf_set_error("lf_hom_mul_rescale: null argument"); return 1; }
   if (ndrop < 1 || ndrop > 2 || level < ndrop) {
     lf_set_error("lf_hom_mul_rescale: cannot drop %d primes at level %d", ndrop, level);
     return 2;
   }
-  if (ct_pitch < level + 1) { lf_set_error("lf_hom_mul_rescale_p: row pitch %d < level + 1", ct_pitch); return 2; }
-  const size_t arow = (size_t)ct_pitch * ctx->N;
+  if (ct1_pitch < level + 1 || ct2_pitch < level + 1) {
+    lf_set_error("lf_hom_mul_rescale_p: row pitch %d / %d < level + 1", ct1_pitch, ct2_pitch);
+    return 2;
+  }
   KsCall c{};
-  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop; c.pitch = ct_pitch;
-  c.x = ct1 + arow; c.x2 = ct2 + arow; c.x_bs = ct_bstride; c.key = rlk; c.key_bs = 0;
-  c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct_bstride;
+  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop;
+  c.pitch = ct1_pitch; c.pitch2 = ct2_pitch; c.sep2 = true;
+  c.x = ct1 + (size_t)ct1_pitch * ctx->N; c.x2 = ct2 + (size_t)ct2_pitch * ctx->N;
+  c.x_bs = ct1_bstride; c.x2_bs = ct2_bstride; c.key = rlk; c.key_bs = 0;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct1_bstride; c.e1_bs = ct2_bstride;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
 }
 
@@ -2196,8 +2209,8 @@ static int shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const 
     const int bpc = B >= 2 * LF_BPC ? LF_BPC : 1;
     dim3 grid(nm * groups, 1, (B + bpc - 1) / bpc);
     const size_t tbs = (size_t)S.m_slots * N;
-    if (c->op == OP_MUL) { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, grid, dim3(S_::TRR), smR, s, 1, c->x, c->x2, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k)); }
-    else { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, grid, dim3(S_::TRR), smR, s, 1, c->x, (const u32*)nullptr, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k)); }
+    if (c->op == OP_MUL) { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, grid, dim3(S_::TRR), smR, s, 1, c->x, c->x2, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, c->x_bstride, 0)); }
+    else { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, grid, dim3(S_::TRR), smR, s, 1, c->x, (const u32*)nullptr, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, (size_t)0, 0)); }
     LF_CHECK_LAUNCH();
     return 0;
   }
@@ -2223,7 +2236,7 @@ static int shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const 
     {   // K_C
       KsInnerArgs A{};
       A.T1 = w.T1; A.x = c->x; A.x2 = c->x2 ? c->x2 : c->x; A.acc = w.acc; A.T2 = w.T2s;
-      A.t1_bs = (size_t)S.beta * S.ext * N; A.x_bs = c->x_bstride; A.acc_bs = (size_t)2 * nm * N;
+      A.t1_bs = (size_t)S.beta * S.ext * N; A.x_bs = c->x_bstride; A.x2_bs = c->x_bstride; A.acc_bs = (size_t)2 * nm * N;
       A.t2_bs = (size_t)2 * P->s_slots * N;
       A.rowk = K->rowk; A.level = level; A.d = K->d; A.beta = S.beta; A.L = K->L; A.alpha = K->n_special;
       A.R = P->n_key_rows; A.nbatch = B; A.pre = 0; A.ext_out = 0; A.fuse_nd = 0; A.t2_rows = P->s_slots;
@@ -2259,7 +2272,8 @@ static int shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const 
     ModDownArgs A{};
     A.T3 = w.T3; A.acc = w.acc; A.out = c->out; A.e0 = c->e0; A.e1 = c->e1;
     A.t3_bs = (size_t)2 * nm * N; A.acc_bs = A.t3_bs; A.out_bs = c->out_bstride; A.e_bs = c->e_bstride;
-    A.scal = K->rowk + 2; A.sstride = 4; A.nt = nm; A.nacc = nm; A.ne = nm;
+    A.e1_bs = c->e_bstride;
+    A.scal = K->rowk + 2; A.sstride = 4; A.nt = nm; A.nacc = nm; A.ne = nm; A.ne1 = nm;
     A.tmap = S.tmap;
     for (int b = 0; b < B; ++b) A.gs[b] = c->galois ? c->galois[b] : 1u;
     A.nbatch = B;

@@ -169,6 +169,14 @@ def test_pitched_views_equal_dense(env):
     assert torch.equal(got.data, want.data) and got.level == want.level == lv - 2
     got, want = be.rescale2(xv), be.rescale2(xd)
     assert torch.equal(got.data, want.data)
+    # operands with different pitches (views of blocks at two levels)
+    z = be.rescale2(y)                                   # level L - 2, pitch L - 1
+    lw = z.level - 2
+    xw, zw = be.drop_to_level(x, lw), be.drop_to_level(z, lw)
+    assert xw.pitched()[1] != zw.pitched()[1]
+    got = be.mul_rescale2(xw, zw)
+    want = be.mul_rescale2(BT.CtBatch(xw.data.contiguous(), xw.scale, lw), BT.CtBatch(zw.data.contiguous(), zw.scale, lw))
+    assert torch.equal(got.data, want.data)
     # a batch of single ciphertexts through the same pitched entry point equals the unbatched op
     one = be.mul_rescale2(be.drop_to_level(ct, lv), be.drop_to_level(ct2, lv))
     assert np.array_equal(one.b.numpy(), be.mul_rescale2(xd, yd).data[0, 0].cpu().numpy())
