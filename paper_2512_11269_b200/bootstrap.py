@@ -620,10 +620,15 @@ class Bootstrapper(CkksCircuit):
         xc = be.conjugate(x)
         re = be.add(x, xc)
         im = be.mul_monomial(be.sub(x, xc), 3 * self.N // 2)   # * (-i) = * X^(3N/2)
-        re = be.add_const(re, self.beta)
-        im = be.add_const(im, self.beta)
+        if hasattr(be, "batch_buffer"):                       # both parts written into one batch
+            buf = be.batch_buffer(2, re.level)
+            be.add_const(re, self.beta, out=buf.data[0])
+            be.add_const(im, self.beta, out=buf.data[1])
+            batch = CtBatch(buf.data, re.scale, re.level)
+        else:
+            batch = be.stack([be.add_const(re, self.beta), be.add_const(im, self.beta)])
         self._mark("conj_split")
-        re, im = be.unstack(self._evalmod(be.stack([re, im])))   # both parts in one batch
+        re, im = be.unstack(self._evalmod(batch))             # both parts in one batch
         self._mark("evalmod")
         y = be.add(re, be.mul_monomial(im, self.N // 2))       # re + i im
         # SlotToCoeff: the first level folds q0/Delta_in, the last lands on out_scale
@@ -752,6 +757,10 @@ class GpuBackend:
         import torch
         return CtBatch(torch.stack([torch.stack([c.b.limbs, c.a.limbs]) for c in cts]),
                        cts[0].scale, cts[0].level)
+
+    def batch_buffer(self, B: int, level: int):
+        import torch
+        return CtBatch(torch.empty((B, 2, level + 1, self.N), dtype=torch.int32, device="cuda"), 1, level)
 
     def unstack(self, x):
         from .poly import Domain, RnsPolynomial, main_ids
@@ -1266,8 +1275,9 @@ class GpuBackend:
         return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
                                  RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale * Fraction(S_p), ct.level)
 
-    def add_const(self, ct, c: float):
-        """ct + c (the constant encoded at the ciphertext's own scale; b only)."""
+    def add_const(self, ct, c: float, out=None):
+        """ct + c (the constant encoded at the ciphertext's own scale; b only).  `out`: a
+        (2, level + 1, N) slot to write into (e.g. one instance of a batch being assembled)."""
         import torch
         from .poly import LF_OP_ADD_SCALAR, Domain, RnsPolynomial, ewise, main_ids
         k = round(Fraction(c) * Fraction(ct.scale))
@@ -1288,9 +1298,10 @@ class GpuBackend:
                     ewise(self.params, LF_OP_ADD_SCALAR, out[i, 1], ct.data[i, 1], rows,
                           scalars=[0] * len(rows))
             return CtBatch(out, ct.scale, ct.level)
-        out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
+        if out is None:
+            out = torch.empty((2, ct.level + 1, self.params.N), dtype=torch.int32, device=ct.b.limbs.device)
         ewise(self.params, LF_OP_ADD_SCALAR, out[0], ct.b.limbs, ids, scalars=self._scalar_rows(ct, k))
-        out[1].copy_(ct.a.limbs)
+        ewise(self.params, LF_OP_ADD_SCALAR, out[1], ct.a.limbs, ids, scalars=[0] * len(ids))
         return self.C.Ciphertext(RnsPolynomial(out[0], Domain.EVAL, ids),
                                  RnsPolynomial(out[1], Domain.EVAL, ids), ct.scale, ct.level)
 
