@@ -50,6 +50,22 @@ def key_rows(level=35, d=4, alpha=9):
     return 2 * min(d, l1) * (l1 + alpha)
 
 
+SHOUP_MAC_PER_CLK_SM = 18.4   # profiles/r01_ubench_imad.log: one Shoup modular MAC per lane
+LINE_BFLY_PER_CLK_SM = 12.1   # profiles/r02_experiments.md: 256-point line code, data on chip
+
+
+def stage_butterflies(level=35, d=4, alpha=9):
+    """NTT butterflies each fused kernel runs per keyswitch (N/2 per stage, 8 stages per pass)."""
+    l1 = level + 1
+    beta = min(d, l1)
+    ext = l1 + alpha
+    conv = beta * ext - l1
+    per_pass = 65536 // 2 * 8
+    return {"modup_in": l1 * per_pass, "modup_bconv": (l1 + conv) * per_pass,
+            "ks_inner": (conv + 2 * alpha) * per_pass, "moddown_bconv": (2 * alpha + 2 * l1) * per_pass,
+            "moddown_out": 2 * l1 * per_pass}
+
+
 def stage_rows(level=35, d=4, alpha=9):
     """Algorithmic rows read+written by each fused kernel ('Kernels'), per
     keyswitch, the evaluation key charged per keyswitch (SURVEY §8d's definition)."""
@@ -865,6 +881,25 @@ def run_ours(args, rank, world):
     except Exception:
         pass
 
+    # the binding resource: NTT butterflies per second against the measured integer ceilings
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    bf = stage_butterflies(level)
+    int_peak = SHOUP_MAC_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+    line_peak = LINE_BFLY_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+    per_stage = {}
+    for name, ms_ in zip(STAGES, stage):
+        tb = bf[name] * Bsz / (ms_ / 1e3) / 1e12 if ms_ > 0 else 0.0
+        per_stage[name] = {"t_butterflies_per_s": tb, "frac": tb / int_peak}
+    ks_bf = sum(bf.values()) / (ms / 1e3 / (Bsz * args.steps)) / 1e12
+    int_roof = {"bound": "int", "unit": "T butterflies/s", "peak": int_peak,
+                "peak_source": "measured Shoup modular MAC rate x 148 SMs x SM clock (profiles/r01_ubench_imad.log)",
+                "line_code_peak": line_peak, "kernel": top,
+                "achieved": per_stage[top]["t_butterflies_per_s"], "frac": per_stage[top]["frac"],
+                "keyswitch": {"butterflies": sum(bf.values()), "achieved": ks_bf, "frac": ks_bf / int_peak,
+                              "frac_of_line_code": ks_bf / line_peak},
+                "stages": per_stage,
+                "note": "NTT butterflies only (BConv MACs run on the tensor cores); every kernel's FMA-heavy pipe is ~50 % busy (profiles/r02_ncu_traffic.json)"}
+
     # e2e: public API, pinned host inputs -> device -> keyswitch -> host, every step
     host_in = torch.empty((Bsz, l1, N), dtype=torch.int32, pin_memory=True)
     host_in.copy_(xs[0].cpu())
@@ -978,6 +1013,7 @@ def run_ours(args, rank, world):
                 "frac": (algorithmic_rows(level) * Bsz - key_rows(level) * (Bsz - 1)) * ROW_BYTES
                         / (ms / args.steps / 1e3) / 1e9 / hbm_peak,
                 "key": "the shared relinearisation key read once per batch"},
+            "int_roofline": int_roof,
             "roofline": {"kernel": top, "bound": "hbm", "achieved": achieved_top, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved_top / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": batch_rows(top) * ROW_BYTES,
