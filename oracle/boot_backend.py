@@ -155,6 +155,26 @@ class OracleBackend:
     def stack(self, cts):
         return ListBatch(cts)
 
+    # batches built from / reduced to single ciphertexts (workloads.py); same results as the
+    # GPU backend's batched kernels, one ciphertext at a time
+    def rot_batch(self, x, steps):
+        return ListBatch(self.rotate_hoisted(x, steps))
+
+    def broadcast(self, x, B):
+        return ListBatch([x] * B)
+
+    def batch_sum(self, x):
+        acc = None
+        for c in x.cts:
+            acc = c if acc is None else O.hom_add(self.P, acc, c)
+        return acc
+
+    def rotate_same(self, x, steps):
+        return ListBatch(self.rotate_many(x.cts, [steps] * len(x.cts)))
+
+    def mul_plain_batch(self, x, pt):
+        return ListBatch([self.mul_plain_sum([(c, pt)]) for c in x.cts])
+
     def unstack(self, x):
         return list(x.cts)
 

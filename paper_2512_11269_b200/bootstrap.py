@@ -683,8 +683,8 @@ class CtBatch:
         d = self.data
         N = d.shape[-1]
         st = d.stride()
-        if st[3] == 1 and st[2] == N and st[1] % N == 0 and st[0] == 2 * st[1]:
-            return st[0], st[1] // N
+        if st[3] == 1 and st[2] == N and st[1] % N == 0 and (st[0] == 2 * st[1] or st[0] == 0):
+            return st[0], st[1] // N           # stride 0: one ciphertext broadcast over the batch
         return None
 
 
@@ -757,6 +757,67 @@ class GpuBackend:
         import torch
         return CtBatch(torch.stack([torch.stack([c.b.limbs, c.a.limbs]) for c in cts]),
                        cts[0].scale, cts[0].level)
+
+    # batches built from / reduced to single ciphertexts (the layer workloads, workloads.py)
+    def rot_batch(self, x, steps):
+        """The rotations of ONE ciphertext by every step (hoisted: one ModUp), as a batch in
+        the order of `steps`; identity steps first."""
+        import torch
+        from . import fused
+        from .fused import ct_block
+        n = self.params.n
+        nid = 0
+        while nid < len(steps) and steps[nid] % n == 0:
+            nid += 1
+        assert all(st % n for st in steps[nid:]), "identity steps must come first"
+        out = torch.empty((len(steps), 2, x.level + 1, self.N), dtype=torch.int32, device="cuda")
+        blk = ct_block(x)
+        for i in range(nid):
+            out[i].copy_(blk)
+        if nid < len(steps):
+            gs = [galois_element_of(self.N, st) for st in steps[nid:]]
+            keys = [self.rk[st % n] for st in steps[nid:]]
+            fused.rotate_hoisted(self.params, x, gs, keys, out=out[nid:])
+        return CtBatch(out, x.scale, x.level)
+
+    def broadcast(self, x, B: int):
+        """One ciphertext as a batch of B (an instance stride of 0: no copies)."""
+        from .fused import ct_block
+        blk = ct_block(x)
+        return CtBatch(blk.unsqueeze(0).expand(B, *blk.shape), x.scale, x.level)
+
+    def batch_sum(self, x):
+        """The sum of a batch's ciphertexts (pairwise halving adds)."""
+        from .poly import LF_OP_ADD
+        x = x.dense()
+        while x.data.shape[0] > 1:
+            B = x.data.shape[0]
+            h = B // 2
+            s = self._b_ewise(LF_OP_ADD, CtBatch(x.data[:h], x.scale, x.level), CtBatch(x.data[h: 2 * h], x.scale, x.level))
+            if B % 2:
+                s = CtBatch(__import__("torch").cat([s.data, x.data[2 * h:]]), x.scale, x.level)
+            x = s
+        return self.unstack(x)[0]
+
+    def rotate_same(self, x, steps: int):
+        """Every instance of a batch rotated by the same step (one batched pipeline)."""
+        from . import fused
+        if steps % self.params.n == 0:
+            return x
+        x = x.dense()
+        B = x.data.shape[0]
+        g = galois_element_of(self.N, steps)
+        keys = self._rot_keys([steps] * B)
+        r = fused.rotate_batch(self.params, x.level, x.data, [g] * B, keys, permuted=self.permuted_keys)
+        return CtBatch(r, x.scale, x.level)
+
+    def mul_plain_batch(self, x, pt):
+        """Every instance times one plaintext (no rescale)."""
+        import torch
+        out = torch.empty((x.data.shape[0], 2, x.level + 1, self.N), dtype=torch.int32, device="cuda")
+        for i, c in enumerate(self.unstack(x)):
+            self.mul_plain_sum([(c, pt)], out=out[i])
+        return CtBatch(out, Fraction(x.scale) * Fraction(pt.scale), x.level)
 
     def batch_buffer(self, B: int, level: int):
         import torch

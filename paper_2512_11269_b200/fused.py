@@ -75,8 +75,9 @@ def rotate(params, ct, g: int, key):
     return _pair(out, main_ids(level))
 
 
-def rotate_hoisted(params, ct, gs, keys):
-    """One shared ModUp of ct.a, then one (inner product, ModDown, sigma_g(b) + .) per key."""
+def rotate_hoisted(params, ct, gs, keys, out=None):
+    """One shared ModUp of ct.a, then one (inner product, ModDown, sigma_g(b) + .) per key;
+    `out`: an (n, 2, level+1, N) contiguous tensor to write into."""
     import ctypes
     ctx = get_context(params)
     level = ct.level
@@ -85,7 +86,8 @@ def rotate_hoisted(params, ct, gs, keys):
     ws = torch.empty(lib.lf_rotate_hoisted_workspace_bytes(ctx.handle, level, n) // 4,
                      dtype=torch.int32, device="cuda")
     c = ct_block(ct)
-    out = torch.empty((n, 2, level + 1, params.N), dtype=torch.int32, device=c.device)
+    if out is None:
+        out = torch.empty((n, 2, level + 1, params.N), dtype=torch.int32, device=c.device)
     karr = (ctypes.c_void_p * n)(*[ctx.check_evk(k).data_ptr() for k in keys])
     _native.check(lib.lf_rotate_hoisted(ctx.handle, level, dptr(c), n, _native.u32_array(gs), karr,
                                         dptr(out), out[0].numel(), dptr(ws), stream_handle()),

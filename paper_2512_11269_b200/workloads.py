@@ -30,7 +30,7 @@ from fractions import Fraction
 
 import numpy as np
 
-from .bootstrap import BootConfig, CkksCircuit, bsgs_apply_plain, bsgs_plan, cheb_interp
+from .bootstrap import BootConfig, CkksCircuit, CtBatch, ListBatch, bsgs_apply_plain, bsgs_plan, cheb_interp
 
 # ---------------------------------------------------------------------------------------
 # slot-domain models (host, float64)
@@ -218,7 +218,11 @@ class TransformerBlock(_Layers):
         return sorted(r)
 
     def _rot(self, x, s):
-        return x if s % self.n == 0 else self.be.rotate_hoisted(x, [s % self.n])[0]
+        if s % self.n == 0:
+            return x
+        if isinstance(x, (CtBatch, ListBatch)):
+            return self.be.rotate_same(x, s % self.n)
+        return self.be.rotate_hoisted(x, [s % self.n])[0]
 
     def _rot_sum(self, x, width):
         """sum over the `width` slots starting at each slot's row (rotate-and-sum, log2 width)."""
@@ -232,6 +236,8 @@ class TransformerBlock(_Layers):
         """x * plaintext(vec) at the working scale (two primes)."""
         l = x.level
         pt = self._pt(tag, vec, l, Fraction(self.q[l]) * self.q[l - 1])
+        if isinstance(x, (CtBatch, ListBatch)):
+            return self.be.rescale2(self.be.mul_plain_batch(x, pt))
         return self.be.rescale2(self.be.mul_plain_sum([(x, pt)]))
 
     def _row_sum_broadcast(self, x):
@@ -246,32 +252,31 @@ class TransformerBlock(_Layers):
         return y
 
     def forward(self, X):
+        """The T score offsets run as ONE batch of T ciphertexts through every kernel: the T
+        rotations of k (and of v) are one hoisted batch, q is broadcast over the batch (an
+        instance stride of 0), the rotate-and-sums, the mask, the exp polynomial and the
+        products are batched launches, and the softmax denominator and the attention output
+        are batch sums.  Residue for residue the same circuit as one offset at a time."""
         be, T, d = self.be, self.T, self.d
         S = Fraction(X.scale)
         q = self.linear(X, self.plans["q"], "wq", 1.0 / (np.sqrt(d) * self.sb))
         k = self.linear(X, self.plans["k"], "wk")
         v = self.linear(X, self.plans["v"], "wv")
+        steps = [(delta * d) % self.n for delta in range(T)]
         # scores for every offset delta: s_delta[t] = <q_t, k_(t+delta)>/(sqrt(d) sb), in [-1, 1]
-        ek, sc = [], None
-        for delta in range(T):
-            prod = self._mulr2(q, self._rot(k, delta * d))
-            prod = self._match(prod, prod.level - 2, S)
-            sdl = self._row_sum_broadcast(self._rot_sum(prod, d))
-            e = self.activation(sdl, self.exp_c, S)        # exp(sb * s)
-            ek.append(e)
-            sc = e if sc is None else be.add(sc, e)
+        prod = self._mulr2(be.broadcast(q, T), be.rot_batch(k, steps))
+        prod = self._match(prod, prod.level - 2, S)
+        sdl = self._row_sum_broadcast(self._rot_sum(prod, d))
+        E = self.activation(sdl, self.exp_c, S)            # exp(sb * s), batch of T
+        sc = be.batch_sum(E)
         # 1/sum through the affine map onto [-1, 1]
         a_, b_ = self.inv_map
-        lv = min(e.level for e in ek)
-        sm = be.drop_to_level(sc, lv)
-        u = be.add_const(self._scale_const(sm, a_), b_)
+        lv = E.level
+        u = be.add_const(self._scale_const(sc, a_), b_)
         inv = self.activation(u, self.inv_c, S)
         # attention output: (sum_delta e_delta * rot(v, delta d)) / sum — the T products run at
         # the exp level, one product by 1/sum at the end
-        acc = None
-        for delta, e in enumerate(ek):
-            t = self._mulr2(be.drop_to_level(e, lv), self._rot(be.drop_to_level(v, lv), delta * d))
-            acc = t if acc is None else be.add(acc, t)
+        acc = be.batch_sum(self._mulr2(E, be.rot_batch(be.drop_to_level(v, lv), steps)))
         acc = self._match(acc, acc.level - 2, S)
         lo = min(acc.level, inv.level)
         acc = self._mulr2(be.drop_to_level(acc, lo), be.drop_to_level(inv, lo))
