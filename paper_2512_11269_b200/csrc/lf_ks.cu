@@ -393,7 +393,7 @@ k_bconv_colpass(BcArgs A, LfDev dv, int kmax, int nbatch) {
 #else
 #define LF_TR(slot) do {} while (0)
 #endif
-template <int L1, int L2, int KB>
+template <int L1, int L2, int KB, bool UEPI>
 __global__ void __launch_bounds__(1024, 1)
 k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   using C = LineCfg<L1>;
@@ -410,6 +410,7 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   __shared__ uint32_t tbase_s;
   __shared__ u32 arrive_cnt;                    // warps done reading TMEM, cumulative over rounds
   __shared__ double invs_sm[16];                // 1 / s_i of the sources (phase 2)
+  __shared__ unsigned char u_sm[UEPI ? 16 * 128 : 1];   // overflow counts when 4k = KB (epilogue term)
 #ifdef LF_BC_TRACE
   __shared__ long long tr_t[8][48];
   __shared__ char tr_c[8][48];
@@ -503,6 +504,7 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   // quarter-warp reads 128 contiguous bytes: conflict-free); any summation order is exact here
   // (the 2^-40 risk window dwarfs the rounding of k <= 11 terms).
   static_assert(E == 2 * TG, "two M-tiles per thread in phase 2");
+  const bool u_epi = UEPI && 4 * k + 1 > KB;       // k = KB / 4 sources fill every K-byte
   {
     double v[2] = {0.0, 0.0};
     const uint4* yc[2] = {reinterpret_cast<const uint4*>(yword(grp, 0)),
@@ -533,7 +535,8 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
         for (int i = 0; i < k; ++i) { yy[i] = *yword(e, i); z &= yy[i] == 0; }
         uj = z ? 0u : bconv_u_exact(yy, B, (u32)r);
       }
-      *yword(e, k) = uj;
+      if (u_epi) u_sm[e * 128 + lt] = (unsigned char)uj;
+      else *yword(e, k) = uj;
     }
   }
   fence_proxy_async_smem();
@@ -577,6 +580,7 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
     LF_TR('m');
     u32 x[E];
     if (active) {
+      const u32 nsu = u_epi ? B.negS[t] : 0u;
 #pragma unroll
       for (int h = 0; h < E / 4; ++h) {
         u32 s[4][4];
@@ -586,7 +590,9 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const u32 lo = s[j][0] + (s[j][1] << 8), z = s[j][2] + (s[j][3] << 8);
-          x[4 * h + j] = reduce64_lazy4((u64)lo + ((u64)z << 16), pk);
+          u64 X = (u64)lo + ((u64)z << 16);
+          if (u_epi) X += (u64)u_sm[(4 * h + j) * 128 + lt] * nsu;
+          x[4 * h + j] = reduce64_lazy4(X, pk);
         }
       }
     }
@@ -1394,7 +1400,7 @@ static int launch_bc(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cud
 
 static int env_int(const char* name, int dflt);
 
-template <int L1, int L2, int KB>
+template <int L1, int L2, int KB, bool UEPI = false>
 static int launch_bc_tc(const LfCtx* ctx, const BcArgs& A, int batch, cudaStream_t s) {
   constexpr int SBO = KB / 16 * 128;
   constexpr size_t ABYTES = (size_t)16 * 16 * SBO + 128;
@@ -1404,7 +1410,7 @@ static int launch_bc_tc(const LfCtx* ctx, const BcArgs& A, int batch, cudaStream
   const int wbytes = (chunk + 7) / 8 * 8 * 256;
   const size_t sm = ABYTES + wbytes + (size_t)8 * smemC_words<L1, 8>() * 4;
   if (sm > 227 * 1024) { lf_set_error("bconv_tc: shared memory %zu too large", sm); return 2; }
-  auto kern = k_bconv_tc<L1, L2, KB>;
+  auto kern = k_bconv_tc<L1, L2, KB, UEPI>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const long nblocks = (long)batch * ((1 << L2) / 8) * A.ngroups * A.tsplit;
   LfDev dv = ctx->dev();
@@ -1415,8 +1421,9 @@ static int launch_bc_tc(const LfCtx* ctx, const BcArgs& A, int batch, cudaStream
 // Column tile width and group count: CW = 8 columns (32-byte row segments) and four thread
 // groups sharing the source tile for the production sizes; narrower tiles for large digit
 // counts (d = 1 style parameter sets) or tiny rings.  At N = 2^16, launches with at most 12
-// sources per group use the compile-time-K kernel.  With byte-split weight tables (k <= 15)
-// the conversion runs on the tensor cores (k_bconv_tc; LF_BC_TC=0 selects the IMAD kernel).
+// sources per group use the compile-time-K kernel.  With byte-split weight tables (k <= 16)
+// the conversion runs on the tensor cores (k_bconv_tc; LF_BC_TC=0 selects the IMAD kernel);
+// k = 16 fills the 64 K-bytes and takes the overflow term in the epilogue (UEPI).
 static int g_bc_engine = -1;     // -1: not read yet; 1: tensor cores when tables allow; 0: IMAD
 static int bc_engine() {
   if (g_bc_engine < 0) g_bc_engine = env_int("LF_BC_TC", 1) ? 1 : 0;
@@ -1426,14 +1433,16 @@ static int bc_engine() {
 template <int L1, int L2>
 static int launch_bc_auto(const LfCtx* ctx, const BcArgs& A, int batch, int kmax, cudaStream_t s) {
   if constexpr (L1 == 8 && L2 == 8) {
-    bool tc = bc_engine() != 0;
+    bool tc = bc_engine() != 0, uepi = false;
     int kb = 0;
     for (int g = 0; g < A.ngroups && tc; ++g) {
       tc = A.g[g].B.w8 != nullptr;
       kb = A.g[g].B.kb > kb ? A.g[g].B.kb : kb;
+      uepi |= 4 * A.g[g].B.k + 1 > 64;
     }
     if (tc && kb == 48) return launch_bc_tc<L1, L2, 48>(ctx, A, batch, s);
-    if (tc && kb == 64) return launch_bc_tc<L1, L2, 64>(ctx, A, batch, s);
+    if (tc && kb == 64 && !uepi) return launch_bc_tc<L1, L2, 64>(ctx, A, batch, s);
+    if (tc && kb == 64) return launch_bc_tc<L1, L2, 64, true>(ctx, A, batch, s);
   }
   constexpr int NCOL = 1 << L2;
   constexpr int CW8 = NCOL >= 8 ? 8 : NCOL;

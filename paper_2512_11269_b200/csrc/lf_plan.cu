@@ -61,11 +61,14 @@ size_t build_w8(Blob& b, const std::vector<u32>& primes, const std::vector<int>&
                 const std::vector<u32>& w, const std::vector<u32>& negS, int& kb) {
   const int m = (int)tgt.size();
   kb = 4 * k + 1 <= 48 ? 48 : 64;
+  // k = 16 fills all 64 K-bytes with sources: the overflow term u * negS is then added in the
+  // kernel's epilogue instead of riding along as K-row 4k
+  const int krows = 4 * k + 1 <= 64 ? 4 * k + 1 : 4 * k;
   const int mp = (m + 1) & ~1;
   std::vector<unsigned char> bytes((size_t)mp * 256, 0);
   for (int t = 0; t < m; ++t) {
     const u32 q = primes[tgt[t]];
-    for (int K = 0; K <= 4 * k; ++K) {
+    for (int K = 0; K < krows; ++K) {
       u32 v;
       if (K == 4 * k) v = negS[t];
       else v = (u32)(((u64)w[(size_t)t * k + K / 4] << (8 * (K % 4))) % q);
@@ -138,7 +141,7 @@ TabRec build_table(Blob& b, const std::vector<u32>& primes, const std::vector<in
   Sw.resize(W, 0);
   v.insert(v.end(), Sw.begin(), Sw.end());
   b.push(v);
-  if (4 * k + 1 <= 64) r.w8off = build_w8(b, primes, tgt, k, wts, negS, r.kb);
+  if (4 * k <= 64) r.w8off = build_w8(b, primes, tgt, k, wts, negS, r.kb);
   return r;
 }
 

@@ -256,3 +256,33 @@ def test_c3_bootstrap_digest_vs_oracle(c3):
     assert dig(out) == meta["sha256"]
     g = BT.GraphedBootstrap(bt, ct)
     assert dig(g(ct)) == meta["sha256"]
+
+
+def test_engines_agree_16_source_moddown():
+    """gen_params(65536, 52, d=4) (the C5 parameters, alpha = 14): the relinearisation fused
+    with a double rescale converts from alpha + 2 = 16 sources, which fill all 64 K-bytes of
+    the tensor-core operand (the overflow term moves to the epilogue).  Tensor-core and IMAD
+    base conversion give identical residues, batched and single."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_11269_b200 as B
+    from paper_2512_11269_b200 import bootstrap as BT
+    p = B.gen_params(65536, 52, d=4, seed=0, scale=2 ** 26)
+    assert p.num_special + 2 == 16
+    sk, pk, rlk = B.keygen(p, seed=3)
+    be = BT.GpuBackend(p, rlk, None, {})
+    rng = np.random.default_rng(2)
+    cts = [B.encrypt(B.encode(rng.uniform(-1, 1, p.n), p), pk, p, np.random.default_rng(i)) for i in range(4)]
+    x, y = be.stack(cts[:2]), be.stack(cts[2:])
+    outs = []
+    for eng in (1, 0):
+        _engine(eng)
+        outs.append((be.mul_rescale2(x, y).data.clone(), ckks_block(be.mul_rescale2(cts[0], cts[1]))))
+    _engine(1)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def ckks_block(ct):
+    import torch
+    return torch.stack([ct.b.limbs, ct.a.limbs]).clone()
