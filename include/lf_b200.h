@@ -139,6 +139,15 @@ int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t
                          int ct2_pitch, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
                          int batch, void* workspace, void* stream);
 
+/* lf_hom_mul_rescale over a LIST of independent operand pairs at one level (instance b: ct1s[b]
+ * with pitch1[b] rows per polynomial, ct2s[b] with pitch2[b]), as one batch: the independent
+ * products of a polynomial evaluation's dependency wave run in one pipeline without gathering
+ * their operands.  out = batch x 2 x (level + 1 - ndrop) rows, instance stride out_bstride. */
+int lf_hom_mul_rescale_list(const lf_ctx* ctx, int level, int ndrop, const uint32_t* const* ct1s,
+                            const int* pitch1, const uint32_t* const* ct2s, const int* pitch2,
+                            const uint32_t* rlk, uint32_t* out, size_t out_bstride, int batch,
+                            void* workspace, void* stream);
+
 /* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
  * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a
  * rotation, 2N-1 for conjugation. */

@@ -412,6 +412,20 @@ class CkksCircuit:
             return be.mul_rescale2(a, b)
         return be.rescale2(be.hom_mul(a, b))
 
+    def _mulr2_many(self, ops):
+        """[_mulr2(a, b) for a, b in ops]; one batched pipeline per level when the backend
+        has one (operand lists, no gathering copies)."""
+        be = self.be
+        if len(ops) > 1 and hasattr(be, "mul_rescale2_many"):
+            out = [None] * len(ops)
+            levels = sorted({a.level for a, _ in ops})
+            for lv in levels:
+                idx = [i for i, (a, _) in enumerate(ops) if a.level == lv]
+                for i, r in zip(idx, be.mul_rescale2_many([ops[i] for i in idx])):
+                    out[i] = r
+            return out
+        return [self._mulr2(a, b) for a, b in ops]
+
     def _cheb_powers(self, u, degree=None):
         """T_1..T_(baby-1) and the giant powers T_baby, T_2baby, ... up to `degree`.
 
@@ -437,25 +451,47 @@ class CkksCircuit:
                 return be.with_scale(x, Fraction(x.scale) / 2)
             return be.add(x, x)
 
-        def double(k):                          # T_2k = 2 T_k^2 - 1
-            x = twice(self._mul2(T[k], T[k]))
-            return be.add_const(x, -1.0)
-
-        def odd(k):                             # T_2k+1 = 2 T_k T_k+1 - T_1
-            if k == 1:                          # T_3 = T_1 (2 T_2 - 1)
-                return self._mul2(T[1], be.add_const(twice(T[2]), -1.0))
-            x = twice(self._mul2(T[k], T[k + 1]))
-            if 2 * k + 1 not in read:
-                T.folded.add(2 * k + 1)
-                return x
-            return be.sub(x, self._match(T[1], x.level, x.scale))
-
-        for m in range(2, g):
-            T[m] = double(m // 2) if m % 2 == 0 else odd(m // 2)
+        # every power is one relinearised product: T_2k = 2 T_k^2 - 1, T_2k+1 = 2 T_k T_k+1 - T_1,
+        # T_3 = T_1 (2 T_2 - 1).  Products whose operands exist form a dependency wave and run
+        # as one batch (mul_rescale2_many); the post-processing is per power.
+        plan = {m: m // 2 for m in range(2, g)}
         G = g
         while G <= degree:
-            T[G] = double(G // 2)
+            plan[G] = G // 2
             G *= 2
+
+        def deps(m):
+            k = plan[m]
+            return (k,) if m % 2 == 0 else ((1, 2) if k == 1 else (k, k + 1))
+
+        pending = sorted(plan)
+        while pending:
+            wave = [m for m in pending if all(dp in T for dp in deps(m))]
+            ops = []
+            for m in wave:
+                k = plan[m]
+                if m % 2 == 0:
+                    a, b = T[k], T[k]
+                elif k == 1:
+                    a, b = T[1], be.add_const(twice(T[2]), -1.0)
+                else:
+                    a, b = T[k], T[k + 1]
+                lv = min(a.level, b.level)
+                ops.append((be.drop_to_level(a, lv), be.drop_to_level(b, lv)))
+            for m, x in zip(wave, self._mulr2_many(ops)):
+                k = plan[m]
+                if m % 2 == 0:
+                    T[m] = be.add_const(twice(x), -1.0)
+                elif k == 1:
+                    T[m] = x
+                else:
+                    x = twice(x)
+                    if m not in read:
+                        T.folded.add(m)
+                        T[m] = x
+                    else:
+                        T[m] = be.sub(x, self._match(T[1], x.level, x.scale))
+            pending = [m for m in pending if m not in wave]
         return T
 
     def _leaf(self, c, T, level, scale):
@@ -1121,6 +1157,59 @@ class GpuBackend:
         b, a = fused.rescale_multi(self.params, x, 2)
         q = self.params.rns_basis
         return self.C.Ciphertext(b, a, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
+
+    def mul_rescale2_many(self, pairs):
+        """[mul_rescale2(x, y) for x, y in pairs] as ONE batch over an operand list
+        (lf_hom_mul_rescale_list): all pairs at one level, all CtBatch or all single."""
+        import ctypes
+        import torch
+        from . import _native
+        from .context import dptr, get_context, stream_handle
+        from .fused import ct_block
+        lv = pairs[0][0].level
+        assert all(x.level == lv and y.level == lv for x, y in pairs)
+        q = self.params.rns_basis
+        bases1, bases2, p1, p2, sizes, scales = [], [], [], [], [], []
+
+        def inst(x):
+            if isinstance(x, CtBatch):
+                pv = x.pitched()
+                if pv is None:
+                    x = x.dense()
+                    pv = (x.data[0].numel(), x.level + 1)
+                return [x.data[i] for i in range(x.data.shape[0])], pv[1], x
+            blk = ct_block(x)
+            return [blk], x.level + 1, x
+
+        keep = []
+        for x, y in pairs:
+            ix, px, x = inst(x)
+            iy, py, y = inst(y)
+            assert len(ix) == len(iy)
+            keep += [x, y] + ix + iy              # operand blocks stay alive until the launch
+            bases1 += [t.data_ptr() for t in ix]
+            bases2 += [t.data_ptr() for t in iy]
+            p1 += [px] * len(ix)
+            p2 += [py] * len(iy)
+            sizes.append(len(ix))
+            scales.append(x.scale * y.scale / q[lv] / q[lv - 1])
+        B = len(bases1)
+        ctx = get_context(self.params)
+        ws = ctx.ks_workspace(lv, min(B, 64))
+        out = torch.empty((B, 2, lv - 1, self.N), dtype=torch.int32, device="cuda")
+        c1 = (ctypes.c_void_p * B)(*bases1)
+        c2 = (ctypes.c_void_p * B)(*bases2)
+        a1 = (ctypes.c_int * B)(*p1)
+        a2 = (ctypes.c_int * B)(*p2)
+        _native.check(_native.lib().lf_hom_mul_rescale_list(ctx.handle, lv, 2, c1, a1, c2, a2,
+                                                            dptr(self.rlk.data), dptr(out), out[0].numel(), B,
+                                                            dptr(ws), stream_handle()), "lf_hom_mul_rescale_list")
+        res, o = [], 0
+        for (x, _), n, sc in zip(pairs, sizes, scales):
+            blk = CtBatch(out[o: o + n], sc, lv - 2)
+            res.append(blk if isinstance(x, CtBatch) else self.unstack(blk)[0])
+            o += n
+        return res
 
     def mul_rescale2(self, x, y):
         """rescale2(hom_mul(x, y)) in one pipeline (lf_hom_mul_rescale, ndrop 2)."""

@@ -37,6 +37,16 @@
   } while (0)
 #define LF_MAXB 64     // batch instances per launch (per-instance key / galois element)
 
+// hom_mul over a list of independent operand pairs (instance b: ct1 at c1[b] with p1[b] rows per
+// polynomial, ct2 at c2[b] with p2[b]): products of different ciphertexts at one level run as ONE
+// batch without gathering them into a contiguous block first.
+struct MulList {
+  const u32* c1[LF_MAXB];
+  const u32* c2[LF_MAXB];
+  int p1[LF_MAXB], p2[LF_MAXB];
+  int on;
+};
+
 LF_DEV void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -61,7 +71,7 @@ template <int L1, int L2, int MODE>
 __global__ void __launch_bounds__(NttShape<L1, L2>::TRR)
 k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restrict__ T0,
            size_t x_bs, size_t t_bs, int nrows, LfDev dv, int rpp, int src_rs, int src_r0, int pbase,
-           int nbatch, int bpc, int pstep, size_t x2_bs, int src_rs2) {
+           int nbatch, int bpc, int pstep, size_t x2_bs, int src_rs2, MulList ml) {
   using S = NttShape<L1, L2>;
   using C = LineCfg<L2>;
   constexpr int GROUPS = (1 << L1) / S::LPCR;
@@ -83,14 +93,20 @@ k_modup_in(const u32* __restrict__ x, const u32* __restrict__ x2, u32* __restric
   for (int b = b0; b < b1; ++b) {
     const size_t off = (size_t)b * x_bs + roff;
     u32 v[C::E];
-    load_row_step2<L2>(v, x + off, tl);
+    if (MODE == 1 && ml.on)          // a1 rows of instance b (row < level + 1: roff = row's offset)
+      load_row_step2<L2>(v, ml.c1[b] + ((size_t)ml.p1[b] << (L1 + L2)) + roff, tl);
+    else
+      load_row_step2<L2>(v, x + off, tl);
     if (MODE == 1) {
       u32 w[C::E];
-      load_row_step2<L2>(w, x2 + (size_t)b * x2_bs + (((size_t)((row / rpp) * src_rs2 + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2)), tl);
+      if (ml.on)
+        load_row_step2<L2>(w, ml.c2[b] + ((size_t)ml.p2[b] << (L1 + L2)) + roff, tl);
+      else
+        load_row_step2<L2>(w, x2 + (size_t)b * x2_bs + (((size_t)((row / rpp) * src_rs2 + src_r0 + row % rpp) << (L1 + L2)) + ((size_t)hi << L2)), tl);
 #pragma unroll
       for (int e = 0; e < C::E; ++e) v[e] = mulmod(v[e], w[e], pk);
     }
-    if (b + 1 < b1) prefetch_l1(x + off + x_bs + (size_t)tl * C::E);
+    if (b + 1 < b1 && !(MODE == 1 && ml.on)) prefetch_l1(x + off + x_bs + (size_t)tl * C::E);
     if (b == b0) {
       tw_bulk_wait(&twbar);
     } else {
@@ -651,6 +667,7 @@ struct KsInnerArgs {
   size_t c_bs, c2_bs;  // instance strides of ct1 / ct2
   int c_ne, c2_ne;     // rows per polynomial of ct1 / ct2
   size_t x2_bs;        // instance stride of x2
+  MulList ml;          // XMODE 1 with ml.on: per-instance operands (x, x2, c1, c2 derived)
   const u32* keyp[LF_MAXB];   // per instance: (d, 2, R, N) key
   u32 gs[LF_MAXB];            // per instance: galois element (GALOIS mode)
   // limb-sharded pipeline (null tmap: one device holds every row): CTA row r of this rank's
@@ -752,7 +769,8 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     } else if (j == own_j) {
       // own row of digit j: (x_t * s_t), permuted by sigma_g for rotations
       const u32 s = A.rowk[4 * t], sp = A.rowk[4 * t + 1];
-      const u32* xr = A.x + b * A.x_bs + ((size_t)r << logN);
+      const u32* xr = (XMODE == 1 && A.ml.on ? A.ml.c1[b] + ((size_t)A.ml.p1[b] << logN) : A.x + b * A.x_bs) +
+                      ((size_t)r << logN);
       if (GALOIS) {
         // the source line, coalesced; sigma_g through the line's slot buffer (GMODE 1)
         load_row_step2<L2>(pc, xr + ((size_t)hs << L2), tl);
@@ -770,7 +788,8 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
           }
         }
       } else {
-        const u32* xr2 = A.x2 + b * A.x2_bs + ((size_t)r << logN);
+        const u32* xr2 = (XMODE == 1 && A.ml.on ? A.ml.c2[b] + ((size_t)A.ml.p2[b] << logN) : A.x2 + b * A.x2_bs) +
+                         ((size_t)r << logN);
         load_row_step2<L2>(pc, xr + ((size_t)hi << L2), tl);
         if (XMODE == 1) {
           u32 w[C::E];
@@ -864,8 +883,9 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
     if (XMODE == 1 && is_main) {
       // + P * (d0, d1) (ckks.py:189-193: d0 = b1 b2, d1 = b1 a2 + a1 b2) before the division
       const u32 pm = A.pmod[2 * t], pmp = A.pmod[2 * t + 1];
-      const u32* c1 = A.c1 + b * A.c_bs;
-      const u32* c2 = A.c2 + b * A.c2_bs;
+      const u32* c1 = A.ml.on ? A.ml.c1[b] : A.c1 + b * A.c_bs;
+      const u32* c2 = A.ml.on ? A.ml.c2[b] : A.c2 + b * A.c2_bs;
+      const int ne1 = A.ml.on ? A.ml.p1[b] : A.c_ne, ne2 = A.ml.on ? A.ml.p2[b] : A.c2_ne;
       const size_t lo = (size_t)hi << L2;
       u32 b1[C::E], b2[C::E], o[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo, tl);
@@ -873,10 +893,10 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
 #pragma unroll
       for (int e = 0; e < C::E; ++e)
         rb[e] = addmod(rb[e], mul_shoup(mulmod(b1[e], b2[e], pk), pm, pmp, pk.q), pk.q);
-      load_row_step2<L2>(o, c2 + ((size_t)(A.c2_ne + t) << logN) + lo, tl);     // a2
+      load_row_step2<L2>(o, c2 + ((size_t)(ne2 + t) << logN) + lo, tl);         // a2
 #pragma unroll
       for (int e = 0; e < C::E; ++e) b1[e] = mulmod(b1[e], o[e], pk);          // b1 a2
-      load_row_step2<L2>(o, c1 + ((size_t)(A.c_ne + t) << logN) + lo, tl);      // a1
+      load_row_step2<L2>(o, c1 + ((size_t)(ne1 + t) << logN) + lo, tl);         // a1
 #pragma unroll
       for (int e = 0; e < C::E; ++e) {
         const u32 d1 = addmod(b1[e], mulmod(o[e], b2[e], pk), pk.q);
@@ -1200,6 +1220,7 @@ struct ModDownArgs {
   int nbatch, bpc;     // instances; instances per CTA (sharing the staged twiddles)
   u32 gs[LF_MAXB];     // per instance galois element (EPI_ROT)
   const int* tmap;     // limb-sharded: storage row r is main prime tmap[r] (null: r)
+  MulList ml;          // EPI_MUL with ml.on: per-instance epilogue operands
 };
 
 template <int L1, int L2, int EPI>
@@ -1254,8 +1275,9 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
     }
     if (EPI == EPI_MUL) {
       // d0 = b1*b2 ; d1 = b1*a2 + a1*b2  (ckks.py:189-193)
-      const u32* c1 = A.e0 + b * A.e_bs;
-      const u32* c2 = A.e1 + b * A.e1_bs;
+      const u32* c1 = A.ml.on ? A.ml.c1[b] : A.e0 + b * A.e_bs;
+      const u32* c2 = A.ml.on ? A.ml.c2[b] : A.e1 + b * A.e1_bs;
+      const int ne1 = A.ml.on ? A.ml.p1[b] : A.ne, ne2 = A.ml.on ? A.ml.p2[b] : A.ne1;
       u32 b1[C::E], b2[C::E], o1[C::E], o2[C::E];
       load_row_step2<L2>(b1, c1 + ((size_t)t << logN) + lo0, tl);
       load_row_step2<L2>(b2, c2 + ((size_t)t << logN) + lo0, tl);
@@ -1268,8 +1290,8 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
           av[e] = addmod(av[e], d0, pk.q);
         }
       } else {
-        load_row_step2<L2>(o1, c1 + ((size_t)(A.ne + t) << logN) + lo0, tl);
-        load_row_step2<L2>(o2, c2 + ((size_t)(A.ne1 + t) << logN) + lo0, tl);
+        load_row_step2<L2>(o1, c1 + ((size_t)(ne1 + t) << logN) + lo0, tl);
+        load_row_step2<L2>(o2, c2 + ((size_t)(ne2 + t) << logN) + lo0, tl);
 #pragma unroll
         for (int e = 0; e < C::E; ++e) {
           u32 d1 = reduce64((u64)b1[e] * o2[e] + (u64)o1[e] * b2[e], pk);
@@ -1501,6 +1523,9 @@ struct KsCall {
   size_t e1s() const { return sep2 ? e1_bs : e_bs; }
   int pitch, pitch2;        // MUL: rows per polynomial of ct1 / ct2 (>= level + 1; 0: level + 1)
   size_t x2_bs, e1_bs;      // MUL: instance strides of a2 / ct2 (used when sep2)
+  const u32* const* c1l;    // MUL over an operand list (instance b0 + b): ct1 / ct2 bases and
+  const u32* const* c2l;    // rows per polynomial (null: strided operands)
+  const int *p1l, *p2l;
   bool sep2;                // ct2 has its own stride and pitch (else those of ct1)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
@@ -1523,6 +1548,14 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
   const int groups = (1 << L1) / S::LPCR;
 
 #define LF_MARK(i) do { if (ev) cudaEventRecord(ev[i], s); } while (0)
+  MulList ml{};
+  if (c.op == OP_MUL && c.c1l) {
+    ml.on = 1;
+    for (int b = 0; b < c.batch; ++b) {
+      ml.c1[b] = c.c1l[c.b0 + b]; ml.c2[b] = c.c2l[c.b0 + b];
+      ml.p1[b] = c.p1l[c.b0 + b]; ml.p2[b] = c.p2l[c.b0 + b];
+    }
+  }
   LF_MARK(0);
   // K_A
   {
@@ -1532,9 +1565,9 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     const int bpc_in = nsh >= 2 * LF_BPC ? LF_BPC : 1;      // instances per CTA (shared twiddles)
     dim3 grid(l1 * groups, 1, (nsh + bpc_in - 1) / bpc_in);
     if (c.op == OP_MUL)
-      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, c.x2s(), l1)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, c.x2, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, c.x2s(), l1, ml)); }
     else
-      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, (size_t)0, 0)); }
+      { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, c.x, nullptr, w.T0, c.x_bs, w.per_sh, l1, dv, l1, 0, 0, 0, nsh, bpc_in, 1, (size_t)0, 0, MulList{})); }
     LF_CHECK_LAUNCH();
   }
   LF_MARK(1);
@@ -1602,6 +1635,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.fuse_nd = nd; A.t2_rows = alpha + nd;
     A.c1 = c.e0; A.c2 = c.e1; A.c_bs = c.e_bs; A.c_ne = c.pitch > 0 ? c.pitch : l1;
     A.c2_bs = c.e1s(); A.c2_ne = c.sep2 ? (c.pitch2 > 0 ? c.pitch2 : l1) : A.c_ne; A.x2_bs = c.x2s();
+    A.ml = ml;
     A.pmod = P->pmod;
     if (c.ext_out) { A.acc = c.out; A.acc_bs = c.out_bs; A.eb = c.e0; A.pmod = P->pmod; }
     for (int b = 0; b < c.batch; ++b) { A.keyp[b] = c.keyp_of(b); A.gs[b] = c.g_of(b); }
@@ -1643,6 +1677,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     A.t3_bs = w.per; A.acc_bs = w.per; A.out_bs = c.out_bs; A.e_bs = c.e_bs; A.e1_bs = c.e1s();
     A.scal = P->rowk + 2; A.sstride = 4; A.nt = nt; A.nacc = l1; A.ne = c.pitch > 0 ? c.pitch : l1;
     A.ne1 = c.sep2 ? (c.pitch2 > 0 ? c.pitch2 : l1) : A.ne;
+    A.ml = ml;
     if (nd) {
       A.scal = P->pqinv[nd - 1] + (size_t)c.level * P->n_main * 2; A.sstride = 2;
       A.dscal = (nd == 1 ? P->qinv : P->qinv2) + (size_t)c.level * P->n_main * 2;
@@ -1683,7 +1718,7 @@ static int rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* ct, 
   u32* T3 = T2 + 2 * (size_t)nd * N;
   {  // row pass of INTT of the dropped rows of b and a
     dim3 grid(2 * nd * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, pitch, nt, nt, batch, 1, 1, (size_t)0, 0)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, ct, nullptr, T2, ct_bs, per, 2 * nd, dv, nd, pitch, nt, nt, batch, 1, 1, (size_t)0, 0, MulList{})); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1727,7 +1762,7 @@ static int moddown_pipeline(const LfCtx* ctx, int level, const u32* in, size_t i
   u32* T3 = T2 + 2 * (size_t)alpha * N;
   {
     dim3 grid(2 * alpha * groups, 1, batch);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1, 1, (size_t)0, 0)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, in, nullptr, T2, in_bs, per, 2 * alpha, dv, alpha, ext, l1, P->L + 1, batch, 1, 1, (size_t)0, 0, MulList{})); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1772,7 +1807,7 @@ static int decompose_pipeline(const LfCtx* ctx, int level, const u32* x, u32* pi
   const int groups = (1 << L1) / S::LPCR;
   {
     dim3 grid(l1 * groups, 1, 1);
-    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1, 1, (size_t)0, 0)); }
+    { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, x, nullptr, w.T0, 0, 0, l1, dv, l1, 0, 0, 0, 1, 1, 1, (size_t)0, 0, MulList{})); }
     LF_CHECK_LAUNCH();
   }
   {
@@ -1905,6 +1940,33 @@ int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t
   c.x = ct1 + (size_t)ct1_pitch * ctx->N; c.x2 = ct2 + (size_t)ct2_pitch * ctx->N;
   c.x_bs = ct1_bstride; c.x2_bs = ct2_bstride; c.key = rlk; c.key_bs = 0;
   c.out = out; c.out_bs = out_bstride; c.e0 = ct1; c.e1 = ct2; c.e_bs = ct1_bstride; c.e1_bs = ct2_bstride;
+  return run_ks(ctx, c, workspace, (cudaStream_t)stream);
+}
+
+int lf_hom_mul_rescale_list(const lf_ctx* ctx, int level, int ndrop, const uint32_t* const* ct1s,
+                            const int* pitch1, const uint32_t* const* ct2s, const int* pitch2,
+                            const uint32_t* rlk, uint32_t* out, size_t out_bstride, int batch,
+                            void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!ct1s || !ct2s || !pitch1 || !pitch2 || !rlk || !out || !workspace || batch < 1) {
+    lf_set_error("lf_hom_mul_rescale_list: bad argument");
+    return 1;
+  }
+  if (ndrop < 1 || ndrop > 2 || level < ndrop) {
+    lf_set_error("lf_hom_mul_rescale_list: cannot drop %d primes at level %d", ndrop, level);
+    return 2;
+  }
+  for (int b = 0; b < batch; ++b)
+    if (!ct1s[b] || !ct2s[b] || pitch1[b] < level + 1 || pitch2[b] < level + 1) {
+      lf_set_error("lf_hom_mul_rescale_list: instance %d: null operand or row pitch < level + 1", b);
+      return 2;
+    }
+  KsCall c{};
+  c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop;
+  c.c1l = ct1s; c.c2l = ct2s; c.p1l = pitch1; c.p2l = pitch2;
+  c.x = ct1s[0] + (size_t)pitch1[0] * ctx->N; c.x2 = ct2s[0] + (size_t)pitch2[0] * ctx->N; c.x_bs = 0;
+  c.key = rlk; c.key_bs = 0;
+  c.out = out; c.out_bs = out_bstride; c.e0 = ct1s[0]; c.e1 = ct2s[0]; c.e_bs = 0;
   return run_ks(ctx, c, workspace, (cudaStream_t)stream);
 }
 
@@ -2218,8 +2280,8 @@ static int shard_phase(const LfCtx* ctx, const LfShardPlan* P, int phase, const 
     const int bpc = B >= 2 * LF_BPC ? LF_BPC : 1;
     dim3 grid(nm * groups, 1, (B + bpc - 1) / bpc);
     const size_t tbs = (size_t)S.m_slots * N;
-    if (c->op == OP_MUL) { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, grid, dim3(S_::TRR), smR, s, 1, c->x, c->x2, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, c->x_bstride, 0)); }
-    else { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, grid, dim3(S_::TRR), smR, s, 1, c->x, (const u32*)nullptr, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, (size_t)0, 0)); }
+    if (c->op == OP_MUL) { lf_smem_optin(k_modup_in<L1, L2, 1>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 1>, grid, dim3(S_::TRR), smR, s, 1, c->x, c->x2, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, c->x_bstride, 0, MulList{})); }
+    else { lf_smem_optin(k_modup_in<L1, L2, 0>, smR); LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, grid, dim3(S_::TRR), smR, s, 1, c->x, (const u32*)nullptr, w.T0s, c->x_bstride, tbs, nm, dv, nm, 0, 0, P->rank, B, bpc, P->k, (size_t)0, 0, MulList{})); }
     LF_CHECK_LAUNCH();
     return 0;
   }
