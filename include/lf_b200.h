@@ -142,11 +142,13 @@ int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t
 /* lf_hom_mul_rescale over a LIST of independent operand pairs at one level (instance b: ct1s[b]
  * with pitch1[b] rows per polynomial, ct2s[b] with pitch2[b]), as one batch: the independent
  * products of a polynomial evaluation's dependency wave run in one pipeline without gathering
- * their operands.  out = batch x 2 x (level + 1 - ndrop) rows, instance stride out_bstride. */
+ * their operands.  add_b (NULL: none): an integer K_b added to every b residue of product b,
+ * i.e. ckks add_const (ckks.py:152-161 with an encoded constant) folded into the epilogue.
+ * out = batch x 2 x (level + 1 - ndrop) rows, instance stride out_bstride. */
 int lf_hom_mul_rescale_list(const lf_ctx* ctx, int level, int ndrop, const uint32_t* const* ct1s,
                             const int* pitch1, const uint32_t* const* ct2s, const int* pitch2,
-                            const uint32_t* rlk, uint32_t* out, size_t out_bstride, int batch,
-                            void* workspace, void* stream);
+                            const int64_t* add_b, const uint32_t* rlk, uint32_t* out,
+                            size_t out_bstride, int batch, void* workspace, void* stream);
 
 /* Galois automorphism g with keyswitch (hom_rotate, ckks.py:197-217: decompose, permute the
  * pieces, inner product, mod_down; b' = sigma_g(b) + ks_b).  g = 5^steps mod 2N for a

@@ -69,7 +69,8 @@ def _load():
                                                 ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int, _u32p, _u32p,
                                                 ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
         "lf_hom_mul_rescale_list": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
-                                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _u32p, _u32p,
+                                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                   ctypes.c_void_p, _u32p, _u32p,
                                                    ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
         "lf_rescale_multi_p": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, ctypes.c_size_t,
                                               ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,

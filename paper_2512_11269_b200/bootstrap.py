@@ -412,19 +412,29 @@ class CkksCircuit:
             return be.mul_rescale2(a, b)
         return be.rescale2(be.hom_mul(a, b))
 
-    def _mulr2_many(self, ops):
-        """[_mulr2(a, b) for a, b in ops]; one batched pipeline per level when the backend
-        has one (operand lists, no gathering copies)."""
+    def _fused_consts(self):
+        return hasattr(self.be, "mul_rescale2_many")
+
+    def _mulr2_many(self, ops, addk=None):
+        """[_mulr2(a, b) (+ addk[i] on b) for a, b in ops]; one batched pipeline per level when
+        the backend has one (operand lists, no gathering copies, the integer addk[i] added in
+        the product's epilogue).  addk is only given when _fused_consts()."""
         be = self.be
-        if len(ops) > 1 and hasattr(be, "mul_rescale2_many"):
+        addk = addk or [None] * len(ops)
+        if hasattr(be, "mul_rescale2_many"):
             out = [None] * len(ops)
             levels = sorted({a.level for a, _ in ops})
             for lv in levels:
                 idx = [i for i, (a, _) in enumerate(ops) if a.level == lv]
-                for i, r in zip(idx, be.mul_rescale2_many([ops[i] for i in idx])):
+                for i, r in zip(idx, be.mul_rescale2_many([ops[i] for i in idx], [addk[i] for i in idx])):
                     out[i] = r
             return out
+        assert not any(k is not None for k in addk)
         return [self._mulr2(a, b) for a, b in ops]
+
+    def _prod_scale(self, a, b):
+        lv = min(a.level, b.level)
+        return Fraction(a.scale) * Fraction(b.scale) / self.q[lv] / self.q[lv - 1]
 
     def _cheb_powers(self, u, degree=None):
         """T_1..T_(baby-1) and the giant powers T_baby, T_2baby, ... up to `degree`.
@@ -467,7 +477,7 @@ class CkksCircuit:
         pending = sorted(plan)
         while pending:
             wave = [m for m in pending if all(dp in T for dp in deps(m))]
-            ops = []
+            ops, addk = [], []
             for m in wave:
                 k = plan[m]
                 if m % 2 == 0:
@@ -478,9 +488,16 @@ class CkksCircuit:
                     a, b = T[k], T[k + 1]
                 lv = min(a.level, b.level)
                 ops.append((be.drop_to_level(a, lv), be.drop_to_level(b, lv)))
-            for m, x in zip(wave, self._mulr2_many(ops)):
+                # 2 x - 1 of a double: the halved declared scale is free and the -1 (encoded at
+                # that scale) is added by the product's epilogue when the backend can
+                half = self._prod_scale(a, b) / 2
+                addk.append(round(-half) if m % 2 == 0 and self._fused_consts() and half >= TWICE_MIN_SCALE
+                            else None)
+            for m, x, kk in zip(wave, self._mulr2_many(ops, addk), addk):
                 k = plan[m]
-                if m % 2 == 0:
+                if m % 2 == 0 and kk is not None:
+                    T[m] = be.with_scale(x, Fraction(x.scale) / 2)
+                elif m % 2 == 0:
                     T[m] = be.add_const(twice(x), -1.0)
                 elif k == 1:
                     T[m] = x
@@ -605,9 +622,11 @@ class Bootstrapper(CkksCircuit):
             raise ValueError("not enough levels for EvalMod")
         scale = Fraction(self.q[t + 1]) * self.q[t + 2]
         y = self._cheb_eval(c, T, t, scale)
-        for sk in self.dbl:
-            y = self._mul2(y, y)
-            y = be.add_const(y, -sk)
+        for sk in self.dbl:                 # c <- c^2 - s_k (the constant in the epilogue when fused)
+            if self._fused_consts():
+                y = self._mulr2_many([(y, y)], [round(Fraction(-sk) * self._prod_scale(y, y))])[0]
+            else:
+                y = be.add_const(self._mul2(y, y), -sk)
         return y
 
     # -- the pipeline ----------------------------------------------------------------
@@ -1158,7 +1177,7 @@ class GpuBackend:
         q = self.params.rns_basis
         return self.C.Ciphertext(b, a, x.scale / q[x.level] / q[x.level - 1], x.level - 2)
 
-    def mul_rescale2_many(self, pairs):
+    def mul_rescale2_many(self, pairs, addk=None):
         """[mul_rescale2(x, y) for x, y in pairs] as ONE batch over an operand list
         (lf_hom_mul_rescale_list): all pairs at one level, all CtBatch or all single."""
         import ctypes
@@ -1194,6 +1213,12 @@ class GpuBackend:
             sizes.append(len(ix))
             scales.append(x.scale * y.scale / q[lv] / q[lv - 1])
         B = len(bases1)
+        kb = None
+        if addk and any(k is not None for k in addk):
+            ks = []
+            for n, k in zip(sizes, addk):
+                ks += [int(k or 0)] * n
+            kb = (ctypes.c_int64 * B)(*ks)
         ctx = get_context(self.params)
         ws = ctx.ks_workspace(lv, min(B, 64))
         out = torch.empty((B, 2, lv - 1, self.N), dtype=torch.int32, device="cuda")
@@ -1201,7 +1226,7 @@ class GpuBackend:
         c2 = (ctypes.c_void_p * B)(*bases2)
         a1 = (ctypes.c_int * B)(*p1)
         a2 = (ctypes.c_int * B)(*p2)
-        _native.check(_native.lib().lf_hom_mul_rescale_list(ctx.handle, lv, 2, c1, a1, c2, a2,
+        _native.check(_native.lib().lf_hom_mul_rescale_list(ctx.handle, lv, 2, c1, a1, c2, a2, kb,
                                                             dptr(self.rlk.data), dptr(out), out[0].numel(), B,
                                                             dptr(ws), stream_handle()), "lf_hom_mul_rescale_list")
         res, o = [], 0

@@ -44,6 +44,7 @@ struct MulList {
   const u32* c1[LF_MAXB];
   const u32* c2[LF_MAXB];
   int p1[LF_MAXB], p2[LF_MAXB];
+  long long addb[LF_MAXB];   // integer added to every b residue of the product (0: none)
   int on;
 };
 
@@ -1289,6 +1290,13 @@ k_moddown_out(ModDownArgs A, LfDev dv) {
           if (A.dscal) d0 = mul_shoup(d0, ds, dsp, pk.q);
           av[e] = addmod(av[e], d0, pk.q);
         }
+        if (A.ml.on && A.ml.addb[b]) {       // + K (mod q): a constant folded into the product
+          const long long K = A.ml.addb[b];
+          u32 kv = reduce64((u64)(K < 0 ? -K : K), pk);
+          if (K < 0 && kv) kv = pk.q - kv;
+#pragma unroll
+          for (int e = 0; e < C::E; ++e) av[e] = addmod(av[e], kv, pk.q);
+        }
       } else {
         load_row_step2<L2>(o1, c1 + ((size_t)(ne1 + t) << logN) + lo0, tl);
         load_row_step2<L2>(o2, c2 + ((size_t)(ne2 + t) << logN) + lo0, tl);
@@ -1526,6 +1534,7 @@ struct KsCall {
   const u32* const* c1l;    // MUL over an operand list (instance b0 + b): ct1 / ct2 bases and
   const u32* const* c2l;    // rows per polynomial (null: strided operands)
   const int *p1l, *p2l;
+  const int64_t* addl;      // MUL list: per-instance constant added to b (null: none)
   bool sep2;                // ct2 has its own stride and pitch (else those of ct1)
   const u32* keyp_of(int b) const { return keylist ? keylist[b0 + b] : key + (size_t)(b0 + b) * key_bs; }
   u32 g_of(int b) const { return glist ? glist[b0 + b] : g; }
@@ -1554,6 +1563,7 @@ static int ks_pipeline(const LfCtx* ctx, const KsCall& c, void* ws, cudaStream_t
     for (int b = 0; b < c.batch; ++b) {
       ml.c1[b] = c.c1l[c.b0 + b]; ml.c2[b] = c.c2l[c.b0 + b];
       ml.p1[b] = c.p1l[c.b0 + b]; ml.p2[b] = c.p2l[c.b0 + b];
+      ml.addb[b] = c.addl ? (long long)c.addl[c.b0 + b] : 0;
     }
   }
   LF_MARK(0);
@@ -1945,8 +1955,8 @@ int lf_hom_mul_rescale_p(const lf_ctx* ctx, int level, int ndrop, const uint32_t
 
 int lf_hom_mul_rescale_list(const lf_ctx* ctx, int level, int ndrop, const uint32_t* const* ct1s,
                             const int* pitch1, const uint32_t* const* ct2s, const int* pitch2,
-                            const uint32_t* rlk, uint32_t* out, size_t out_bstride, int batch,
-                            void* workspace, void* stream) {
+                            const int64_t* add_b, const uint32_t* rlk, uint32_t* out, size_t out_bstride,
+                            int batch, void* workspace, void* stream) {
   if (int e = ks_check(ctx, level)) return e;
   if (!ct1s || !ct2s || !pitch1 || !pitch2 || !rlk || !out || !workspace || batch < 1) {
     lf_set_error("lf_hom_mul_rescale_list: bad argument");
@@ -1963,7 +1973,7 @@ int lf_hom_mul_rescale_list(const lf_ctx* ctx, int level, int ndrop, const uint3
     }
   KsCall c{};
   c.level = level; c.batch = batch; c.op = OP_MUL; c.rescale_nd = ndrop;
-  c.c1l = ct1s; c.c2l = ct2s; c.p1l = pitch1; c.p2l = pitch2;
+  c.c1l = ct1s; c.c2l = ct2s; c.p1l = pitch1; c.p2l = pitch2; c.addl = add_b;
   c.x = ct1s[0] + (size_t)pitch1[0] * ctx->N; c.x2 = ct2s[0] + (size_t)pitch2[0] * ctx->N; c.x_bs = 0;
   c.key = rlk; c.key_bs = 0;
   c.out = out; c.out_bs = out_bstride; c.e0 = ct1s[0]; c.e1 = ct2s[0]; c.e_bs = 0;
