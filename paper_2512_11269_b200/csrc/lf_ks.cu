@@ -425,7 +425,6 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   extern __shared__ __align__(1024) unsigned char smb[];
   __shared__ uint64_t mbar;                     // MMA completion of the current round
   __shared__ uint32_t tbase_s;
-  __shared__ u32 arrive_cnt;                    // warps done reading TMEM, cumulative over rounds
   __shared__ double invs_sm[16];                // 1 / s_i of the sources (phase 2)
   __shared__ unsigned char u_sm[UEPI ? 16 * 128 : 1];   // overflow counts when 4k = KB (epilogue term)
 #ifdef LF_BC_TRACE
@@ -471,7 +470,6 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
     if (threadIdx.x < 32) tmem_alloc(&tbase_s, 512);
     if (threadIdx.x == 0) {
       mbar_init(&mbar, 1);
-      arrive_cnt = 0;
     }
     if (threadIdx.x < k) invs_sm[threadIdx.x] = B.inv_s[threadIdx.x];
   }
@@ -579,12 +577,11 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
   if (threadIdx.x == 0 && nrounds > 0) issue(0);
 
   // phase 3: per round, group g takes target t0 + 8 r + g: S_b from TMEM -> X mod t (lazy) ->
-  // NTT column pass -> destination row.  No CTA barrier per round: every warp, once its TMEM
-  // reads of round r completed, arrives on a shared counter (acq_rel), and the LAST warp to
-  // arrive issues the MMAs of round r + 1 into the freed accumulators, so the groups drift
-  // freely instead of waiting for the slowest one before their NTT.
+  // NTT column pass -> destination row.  A CTA barrier after the TMEM reads frees the
+  // accumulators for round r + 1's MMAs.  (Letting the last warp to arrive on an acq_rel
+  // shared counter issue them instead, without a barrier, gave no speed-up and produced wrong
+  // accumulators in rare launches: the tcgen05 ordering needs the full barrier.)
   const uint32_t tlane = tmem + ((uint32_t)(32 * ((threadIdx.x / 32) % 4)) << 16) + 4 * grp;
-  const int nwarps = blockDim.x / 32;
 #pragma unroll 1
   for (int r = 0; r < nrounds; ++r) {
     const int t = t0 + TG * r + grp;
@@ -614,15 +611,11 @@ k_bconv_tc(BcArgs A, LfDev dv, int nbatch, int wbytes) {
       }
     }
     tc_fence_before();
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      const u32 old = atomic_add_acq_rel_smem(&arrive_cnt, 1u);
-      if (old == (u32)(nwarps * (r + 1) - 1) && r + 1 < nrounds) {   // last reader of round r
-        tc_fence_after();
-        issue(r + 1);
-      }
+    __syncthreads();                                     // TMEM free for the next round
+    if (threadIdx.x == 0 && r + 1 < nrounds) {
+      tc_fence_after();
+      issue(r + 1);
     }
-    __syncwarp();
     LF_TR('d');
     if (active) {
       fwd_line<L1, 4>(x, 1u, TwGlobalT<L1>{dv.twfT + ((size_t)B.tgt_pi[t] << logN), 1u, 1}, pk.q, X, tl, addr, gsync);

@@ -79,13 +79,4 @@ LF_UMMA_DEV void tmem_ld4(uint32_t taddr, uint32_t& a, uint32_t& b, uint32_t& c,
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(taddr));
 }
-// Shared-memory counter increment with acquire-release semantics at CTA scope: orders this
-// warp's completed TMEM reads (tcgen05.fence::before_thread_sync) before the last arriver's
-// MMA issue (tcgen05.fence::after_thread_sync).
-LF_UMMA_DEV uint32_t atomic_add_acq_rel_smem(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
-               : "=r"(old) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-  return old;
-}
 LF_UMMA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
