@@ -180,3 +180,31 @@ def test_pitched_views_equal_dense(env):
     # a batch of single ciphertexts through the same pitched entry point equals the unbatched op
     one = be.mul_rescale2(be.drop_to_level(ct, lv), be.drop_to_level(ct2, lv))
     assert np.array_equal(one.b.numpy(), be.mul_rescale2(xd, yd).data[0, 0].cpu().numpy())
+
+
+def test_mul_rescale_list_equals_pairs(env):
+    """lf_hom_mul_rescale_list over operand pairs of different blocks, pitches and batch sizes
+    (with and without an epilogue constant) equals the pairs one at a time (+ add_const)."""
+    import torch
+    B, O, p, P, sk, rlk, ko, rk, rko, steps, ct, cto = env
+    from fractions import Fraction
+    from paper_2512_11269_b200 import bootstrap as BT
+    be = BT.GpuBackend(p, rlk, None, rk)
+    pk = B.keygen(p, seed=11)[1]
+    cts = [B.encrypt(B.encode(np.random.default_rng(i).uniform(-1, 1, p.n), p), pk, p, np.random.default_rng(10 + i))
+           for i in range(4)]
+    hi = be.stack(cts[:2])                                # level L block
+    lo = be.rescale2(be.stack(cts[2:]))                   # level L - 2 block, other pitch
+    lv = lo.level - 1
+    x1, y1 = be.drop_to_level(hi, lv), be.drop_to_level(lo, lv)
+    x2, y2 = be.drop_to_level(lo, lv), be.drop_to_level(lo, lv)
+    single = (be.drop_to_level(cts[0], lv), be.drop_to_level(cts[3], lv))
+    pairs = [(x1, y1), (x2, y2)]
+    K = -12345678901
+    got = be.mul_rescale2_many(pairs, [None, K])
+    want0 = be.mul_rescale2(x1, y1)
+    want1 = be.add_const(be.mul_rescale2(x2, y2), Fraction(K) / Fraction(be.mul_rescale2(x2, y2).scale))
+    assert torch.equal(got[0].data, want0.data) and torch.equal(got[1].data, want1.data)
+    g1 = be.mul_rescale2_many([single])[0]
+    w1 = be.mul_rescale2(*single)
+    assert np.array_equal(g1.b.numpy(), w1.b.numpy()) and np.array_equal(g1.a.numpy(), w1.a.numpy())
