@@ -523,7 +523,29 @@ def batch_sweep(params, level, rlk, dev, batches=(1, 8), steps=5):
             b.record()
             torch.cuda.synchronize()
             ms += a.elapsed_time(b)
-        out[str(B)] = {"keyswitch_us": ms / steps / B * 1e3}
+        rec = {"keyswitch_us": ms / steps / B * 1e3}
+        if B == 1:
+            # latency of one keyswitch replayed from a CUDA graph (no host launch gaps)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                fused.keyswitch_batch(params, level, x, rlk, out=o, ws=ws)
+            torch.cuda.current_stream().wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                fused.keyswitch_batch(params, level, x, rlk, out=o, ws=ws)
+            gms = []
+            for i in range(steps):
+                flush.fill_(i)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                graph.replay()
+                b.record()
+                torch.cuda.synchronize()
+                gms.append(a.elapsed_time(b))
+            rec["keyswitch_us_graph"] = statistics.median(gms) * 1e3
+            del graph
+        out[str(B)] = rec
         del x, o, ws
     return out
 
