@@ -1,3 +1,6 @@
+"""Reproducer for the round-2 k_bconv_tc regression (profiles/r02_experiments.md): a ResNet
+block at the C3 parameters, then batch-128 double rescales at the C5 parameters, compared
+across repeats.  python tools/repro_bconv_history.py prior"""
 import os, sys, gc
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
