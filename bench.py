@@ -454,6 +454,8 @@ def transformer_block_latency(reps=2):
     out, eager_ms, ms = _graph_latency(be, blk.forward, ct, reps)
     got = B.decrypt(out, sk, p)[: T * d].real.reshape(T, d)
     err = float(np.abs(got - blk.reference(X)).max())
+    del blk
+    sharded = shard_mul_emulation(p, 48, be.rlk)
     key_gb = nkeys * 2 * p.ks.d * (p.max_level + 1 + p.num_special) * p.N * 4 / 1e9
     return {"ms": ms, "ms_eager": eager_ms, "reps": reps,
             "workload": "single-head transformer block, 128 tokens x 64 features: 6 BSGS projections, "
@@ -462,6 +464,7 @@ def transformer_block_latency(reps=2):
             "rotation_keys": nkeys, "key_gb_per_gpu_1": key_gb,
             "key_gb_per_gpu_sharded_8": key_gb / 8,
             "max_err_vs_float_block": err,
+            "sharded_products_emulated": sharded,
             "paper_context": "full BERT-Base (12 layers x 12 heads, 768 hidden) 28.3 s on 1xB200 (PAPER.md:695)",
             "setup_s": setup}
 
@@ -648,6 +651,42 @@ def secondary_keyswitch(dev, B=32, steps=5):
     return {"config": "gen_params(65536, 24, d=3): 25 main + 9 special, ext 34", "batch": B,
             "keyswitch_us": us, "ops_per_s": 1e6 / us, "algorithmic_bytes": rows_alg * N * 4,
             "hbm_gbs": rows_alg * N * 4 / (us * 1e-6) / 1e9}
+
+
+def shard_mul_emulation(params, level, rlk, batch=64, ks=(1, 2, 4, 8), reps=2):
+    """The C5 block's dominant operation on the limb-sharded path: a batch of `batch`
+    relinearised products (half the 128 score offsets) at the block's parameters, each rank's share
+    of the fused pipeline run rank by rank on one GPU (k = 1: the unsharded pipeline through
+    the same engine).  Per-rank device time, max over ranks; NVLink gathers not timed."""
+    import torch
+    from paper_2512_11269_b200.shard import ShardEngine
+    l1, N = level + 1, params.N
+    q = torch.tensor(params.rns_basis[:l1], dtype=torch.int64, device="cuda")[:, None]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    c1 = (torch.randint(0, 2 ** 62, (batch, 2, l1, N), device="cuda", generator=g, dtype=torch.int64) % q).to(torch.int32)
+    c2 = (torch.randint(0, 2 ** 62, (batch, 2, l1, N), device="cuda", generator=g, dtype=torch.int64) % q).to(torch.int32)
+    out = {}
+    for k in ks:
+        eng = [ShardEngine(params, k, r) for r in range(k)]
+        calls = [e.hom_mul_call(level, e.shard_rows(c1, level), e.shard_rows(c2, level), e.shard_key(rlk))[0]
+                 for e in eng]
+        per = [0.0] * k
+        for it in range(reps + 1):
+            for r, (e, c) in enumerate(zip(eng, calls)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for ph in range(3):
+                    e.phase(ph, c, level, batch)
+                b.record()
+                torch.cuda.synchronize()
+                if it:
+                    per[r] += a.elapsed_time(b) / reps
+        out[str(k)] = {"per_rank_us_per_product": max(per) / batch * 1e3,
+                       "key_rows_per_gpu": eng[0].info(params.max_level)["n_key_rows"]}
+        del eng, calls
+    out["note"] = (f"relinearised products (hom_mul, batches of {batch}: the sharded pipeline's limit) at level "
+                   f"{level}, the C5 score products; ranks emulated one by one on one B200, all-gathers not timed")
+    return out
 
 
 def shard_emulation(params, level, rlk, dev, batch=32, ks=(2, 4, 8), reps=3):
