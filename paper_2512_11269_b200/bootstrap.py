@@ -553,21 +553,34 @@ class CkksCircuit:
         return G
 
     def _cheb_eval(self, c, T, level, scale):
+        """sum_k c_k T_k at exactly (level, scale) by Chebyshev division: c = q T_G + r with
+        the q-part one level-pair higher, multiplied by T_G.  When the remainder r is itself
+        split (r = q' T_G' + r'), its product q'·T_G' sits at the same level as q·T_G and both
+        run as ONE batched relinearised product (`_mulr2_many`)."""
         be = self.be
         g = self.cfg.baby
         c = np.trim_zeros(np.asarray(c, dtype=np.float64), "b")
         if len(c) <= g:
             return self._leaf(c, T, level, scale)
-        G = self._giant_for(len(c) - 1)
-        q, r = cheb_divmod(c, G)
         m = level + 2
-        TG = be.drop_to_level(T[G], m)
-        q_scale = Fraction(scale) * self.q[m] * self.q[m - 1] / Fraction(TG.scale)
-        qc = self._cheb_eval(q, T, m, q_scale)
+
+        def split(cc):
+            G = self._giant_for(len(cc) - 1)
+            q, r = cheb_divmod(cc, G)
+            TG = be.drop_to_level(T[G], m)
+            q_scale = Fraction(scale) * self.q[m] * self.q[m - 1] / Fraction(TG.scale)
+            return self._cheb_eval(q, T, m, q_scale), TG, r
+
+        qc, TG, r = split(c)
+        r = np.trim_zeros(np.asarray(r, dtype=np.float64), "b")
+        if len(r) > g:
+            qc2, TG2, r2 = split(r)
+            prod, prod2 = self._mulr2_many([(qc, TG), (qc2, TG2)])
+            assert prod.level == prod2.level == level and prod.scale == prod2.scale == scale
+            return be.add(prod, be.add(prod2, self._cheb_eval(r2, T, level, scale)))
         prod = self._mulr2(qc, TG)
         assert prod.level == level and prod.scale == scale
-        rc = self._cheb_eval(r, T, level, scale)
-        return be.add(prod, rc)
+        return be.add(prod, self._cheb_eval(r, T, level, scale))
 
 
 class Bootstrapper(CkksCircuit):
