@@ -289,6 +289,13 @@ int lf_rotate_hoisted_ext(const lf_ctx* ctx, int level, const uint32_t* ct, int 
 size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch);
 int lf_moddown_ext(const lf_ctx* ctx, int level, const uint32_t* in_ext, size_t in_bstride,
                    uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream);
+
+/* lf_moddown_ext followed by ndrop in {1, 2} rescales (ckks.py:220-225), bit for bit, as ONE
+ * exact floor division by P q_level [q_level-1] (the tables of lf_hom_mul_rescale): out =
+ * batch x 2 x (level + 1 - ndrop) rows; workspace as lf_moddown_ext. */
+int lf_moddown_ext_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* in_ext,
+                           size_t in_bstride, uint32_t* out, size_t out_bstride, int batch,
+                           void* workspace, void* stream);
 /* lf_ptmac over rows with arbitrary primes (prime_idx: HOST array, nrows entries). */
 int lf_ptmac_rows(const lf_ctx* ctx, uint32_t* out, int nrows, const int32_t* prime_idx, int nterm,
                   const uint32_t* const* b, const uint32_t* const* a, const uint32_t* const* pt,

@@ -103,7 +103,9 @@ class OracleBackend:
             out.append(O.Ct(b, aa, ct.scale, ct.level))
         return out
 
-    def bsgs_combine_ext(self, groups):
+    def bsgs_combine_ext(self, groups, nres=0):
+        """Per giant: sum over the extended basis, mod_down, then `nres` rescales BEFORE the
+        giant rotation (the GPU backend fuses the three into one division), rotate, sum."""
         P = self.P
         acc = None
         for st, pairs in groups:
@@ -113,6 +115,8 @@ class OracleBackend:
                 s = t if s is None else O.hom_add(P, s, t)
             ids = P.main_ids(s.level)
             c = O.Ct(O.mod_down(P, s.b, ids), O.mod_down(P, s.a, ids), s.scale, s.level)
+            for _ in range(nres):
+                c = self.rescale(c)
             if st % P.n:
                 c = O.hom_rotate(P, c, st, self.rk[st % P.n])
             acc = c if acc is None else O.hom_add(P, acc, c)

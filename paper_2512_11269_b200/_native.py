@@ -72,6 +72,8 @@ def _load():
                                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                    ctypes.c_void_p, _u32p, _u32p,
                                                    ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+        "lf_moddown_ext_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, ctypes.c_size_t,
+                                                  _u32p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
         "lf_rescale_multi_p": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, ctypes.c_size_t,
                                               ctypes.c_int, _u32p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
                                               ctypes.c_void_p]),

@@ -263,6 +263,7 @@ def cheb_divmod(c: np.ndarray, G: int):
     return q, r
 
 
+EARLY_RESCALE_MIN_SCALE = 2 ** 40   # BSGS giants rescaled before their rotations only above this scale
 TWICE_MIN_SCALE = 2 ** 20      # lowest declared scale the free Chebyshev doubling may leave (default
                                # degree 31: T_16 at ~2^37, untouched)
 
@@ -356,6 +357,18 @@ class CkksCircuit:
         l = ct.level
         S_p = Fraction(S_p)
         lazy = self.cfg.lazy_moddown and hasattr(be, "rotate_hoisted_ext")
+        # The giants' rescale can run before their rotations (fused into the giants' ModDown)
+        # only while the rescaled scale stays large: a rotation's keyswitch noise is absolute,
+        # so rotating at a ~2^26 scale would cost precision (SlotToCoeff keeps the old order).
+        s_out = Fraction(ct.scale) * S_p
+        for i in range(nres):
+            s_out /= self.q[l - i]
+        early = nres if s_out >= EARLY_RESCALE_MIN_SCALE else 0
+
+        def finish(acc):
+            if early:
+                return acc
+            return be.rescale2(acc) if nres == 2 else be.rescale(acc)
         if lazy and hasattr(be, "bsgs_fused_ext"):
             # the backend fuses the baby rotations with the giant-step plaintext sums
             groups = []
@@ -365,9 +378,9 @@ class CkksCircuit:
                                       S_p, ext=True))
                          for b in plan.baby if b // plan.unit in terms]
                 groups.append(((k * plan.g * plan.unit) % self.n, pairs))
-            acc = be.bsgs_fused_ext(ct, groups)
+            acc = be.bsgs_fused_ext(ct, groups, early)
             if acc is not None:
-                return be.rescale2(acc) if nres == 2 else be.rescale(acc)
+                return finish(acc)
         if lazy:
             nz = [b for b in plan.baby if b % self.n]
             ext = dict(zip(nz, be.rotate_hoisted_ext(ct, nz))) if nz else {}
@@ -385,7 +398,9 @@ class CkksCircuit:
                     pt = self._pt((tag, k, bu, lazy), terms[bu] * const, l, S_p, ext=lazy)
                     pairs.append(((ext if lazy else rmap)[b], pt))
             groups.append(((k * plan.g * plan.unit) % self.n, pairs))
-        acc = be.bsgs_combine_ext(groups) if lazy else be.bsgs_combine(groups)
+        if lazy:
+            return finish(be.bsgs_combine_ext(groups, early))
+        acc = be.bsgs_combine(groups)
         return be.rescale2(acc) if nres == 2 else be.rescale(acc)
 
     def _match(self, ct, level, scale):
@@ -982,7 +997,7 @@ class GpuBackend:
                       "lf_rotate_hoisted_ext")
         return [ExtCt(out[i], ct.scale, level) for i in range(n)]
 
-    def bsgs_fused_ext(self, ct, groups):
+    def bsgs_fused_ext(self, ct, groups, nres=0):
         """groups: [(giant shift, [(baby step, extended plaintext)])].  All baby rotations and
         every giant step's plaintext sum in one lf_bsgs_ext pipeline, then one batched
         mod_down and the giant rotations (rotate_and_sum).  None when the plan exceeds the
@@ -1002,10 +1017,10 @@ class GpuBackend:
             inner = [self._bsgs_inner(ct, c) for c in chunks]
             pt0 = groups[0][1][0][1]
             return self._moddown_and_sum(torch.cat(inner), [st for st, _ in groups], ct.scale * pt0.scale,
-                                         ct.level)
+                                         ct.level, nres)
         inner = self._bsgs_inner(ct, groups)
         pt0 = next(pt for _, pairs in groups for _, pt in pairs)
-        return self._moddown_and_sum(inner, [st for st, _ in groups], ct.scale * pt0.scale, ct.level)
+        return self._moddown_and_sum(inner, [st for st, _ in groups], ct.scale * pt0.scale, ct.level, nres)
 
     def _bsgs_inner(self, ct, groups):
         """lf_bsgs_ext for <= 4 giant groups: (G, 2, ext, N) extended-basis giant sums."""
@@ -1040,9 +1055,10 @@ class GpuBackend:
                                       karr, G, parr, dptr(inner), dptr(ws), stream_handle()), "lf_bsgs_ext")
         return inner
 
-    def _moddown_and_sum(self, inner, shifts, scale, level):
-        """ONE batched mod_down of the giant steps' extended sums (lf_moddown_ext), then the
-        giant rotations and the final sum (rotate_and_sum)."""
+    def _moddown_and_sum(self, inner, shifts, scale, level, nres=0):
+        """ONE batched mod_down of the giant steps' extended sums (lf_moddown_ext; with nres
+        rescales fused into the same division, lf_moddown_ext_rescale), then the giant
+        rotations and the final sum (rotate_and_sum)."""
         import torch
         from . import _native
         from .context import dptr, get_context, stream_handle
@@ -1051,20 +1067,30 @@ class GpuBackend:
         lib = _native.lib()
         G = inner.shape[0]
         N = self.params.N
-        out = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
         ws = torch.empty(lib.lf_moddown_workspace_bytes(ctx.handle, level, G) // 4, dtype=torch.int32,
                          device="cuda")
-        _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(out),
-                                         out[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
+        if nres:
+            q = self.params.rns_basis
+            out = torch.empty((G, 2, level + 1 - nres, N), dtype=torch.int32, device="cuda")
+            _native.check(lib.lf_moddown_ext_rescale(ctx.handle, level, nres, dptr(inner), inner[0].numel(),
+                                                     dptr(out), out[0].numel(), G, dptr(ws), stream_handle()),
+                          "lf_moddown_ext_rescale")
+            for i in range(nres):
+                scale = Fraction(scale) / q[level - i]
+            level -= nres
+        else:
+            out = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
+            _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(out),
+                                             out[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
         ids = main_ids(level)
         cts = [self.C.Ciphertext(RnsPolynomial(out[i, 0], Domain.EVAL, ids),
                                  RnsPolynomial(out[i, 1], Domain.EVAL, ids), scale, level) for i in range(G)]
         return self.rotate_and_sum(list(zip(shifts, cts)), batch=out)
 
-    def bsgs_combine_ext(self, groups):
+    def bsgs_combine_ext(self, groups, nres=0):
         """Per giant step: sum_b ext_b * pt_{k,b} over the extended basis (lf_ptmac_rows) into one
-        batch, ONE batched mod_down of all giant steps (lf_moddown_ext), then the batched giant
-        rotations and the final sum (rotate_and_sum)."""
+        batch, ONE batched mod_down of all giant steps (lf_moddown_ext; + nres rescales in the
+        same division), then the batched giant rotations and the final sum (rotate_and_sum)."""
         import torch
         from . import _native
         from .context import dptr, get_context, stream_handle
@@ -1088,15 +1114,7 @@ class GpuBackend:
             _native.check(lib.lf_ptmac_rows(ctx.handle, ctypes_void_p(inner[i].data_ptr()), ext, pidx, n,
                                             bp, ap, pp, stream_handle()), "lf_ptmac_rows")
         scale = x0.scale * groups[0][1][0][1].scale
-        out = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
-        ws = torch.empty(lib.lf_moddown_workspace_bytes(ctx.handle, level, G) // 4, dtype=torch.int32,
-                         device="cuda")
-        _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(out),
-                                         out[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
-        ids = main_ids(level)
-        cts = [self.C.Ciphertext(RnsPolynomial(out[i, 0], Domain.EVAL, ids),
-                                 RnsPolynomial(out[i, 1], Domain.EVAL, ids), scale, level) for i in range(G)]
-        return self.rotate_and_sum([(st, c) for (st, _), c in zip(groups, cts)], batch=out)
+        return self._moddown_and_sum(inner, [st for st, _ in groups], scale, level, nres)
 
     def rotate_and_sum(self, items, batch=None):
         """sum_k rot_{s_k}(ct_k): the rotated ones in one lf_rotate_batch pipeline (they must be

@@ -1872,6 +1872,65 @@ static int run_ks(const lf_ctx* ctx, const KsCall& c, void* ws, cudaStream_t s,
   return 0;
 }
 
+// ModDown of extended-basis ciphertexts fused with a rescale by nd in {1, 2} primes: ONE exact
+// floor division by P q_level [q_level-1] (the K.dr tables of lf_hom_mul_rescale), bit-identical
+// to lf_moddown_ext followed by nd rescales.  The INTT row pass puts each polynomial's alpha
+// special rows and its nd top main rows into T2 in the tables' source order.
+template <int L1, int L2>
+static int moddown_rescale_pipeline(const LfCtx* ctx, int level, int nd, const u32* in, size_t in_bs,
+                                    u32* out, size_t out_bs, int batch, void* ws, cudaStream_t s) {
+  using S = NttShape<L1, L2>;
+  const LfKsPlan* P = ctx->ks;
+  const KsLevelPlan& K = P->lv[level];
+  const int l1 = level + 1, alpha = P->n_special, ext = l1 + alpha, nt = l1 - nd;
+  const size_t N = ctx->N;
+  const LfDev dv = ctx->dev();
+  const size_t smR = rowpass_smem_bytes<L1, L2>(0);
+  const int groups = (1 << L1) / S::LPCR;
+  u32* T2 = (u32*)ws;                              // per instance: 2 (alpha + nd) rows, then T3: 2 nt
+  const size_t per = (2 * (size_t)(alpha + nd) + 2 * (size_t)nt) * N;
+  u32* T3 = T2 + 2 * (size_t)(alpha + nd) * N;
+  lf_smem_optin(k_modup_in<L1, L2, 0>, smR);
+  for (int p = 0; p < 2; ++p) {
+    const u32* src = in + (size_t)p * ext * N;
+    u32* t2p = T2 + (size_t)p * (alpha + nd) * N;
+    {   // specials: input rows l+1 .. l+alpha, primes L+1 ..
+      dim3 grid(alpha * groups, 1, batch);
+      LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, src, nullptr, t2p, in_bs, per,
+                                alpha, dv, alpha, 0, l1, P->L + 1, batch, 1, 1, (size_t)0, 0, MulList{}));
+    }
+    {   // the nd top main rows l-nd+1 .. l
+      dim3 grid(nd * groups, 1, batch);
+      LF_LAUNCH_CHECK(lf_launch(k_modup_in<L1, L2, 0>, dim3(grid), dim3(S::TRR), smR, s, 1, src, nullptr,
+                                t2p + (size_t)alpha * N, in_bs, per, nd, dv, nd, 0, l1 - nd, l1 - nd, batch, 1, 1,
+                                (size_t)0, 0, MulList{}));
+    }
+    LF_CHECK_LAUNCH();
+  }
+  {
+    BcArgs A{};
+    A.src = T2; A.dst = T3; A.src_bs = per; A.dst_bs = per;
+    A.ngroups = 2;
+    A.g[0] = K.dr[nd - 1][0];
+    A.g[1] = K.dr[nd - 1][1];
+    A.tsplit = bc_tsplit(2, batch, (1 << L2) / 8, nt);
+    if (int e = launch_bc_auto<L1, L2>(ctx, A, batch, alpha + nd, s)) return e;
+  }
+  {
+    ModDownArgs A{};
+    A.T3 = T3; A.acc = in; A.out = out; A.e0 = nullptr; A.e1 = nullptr;
+    A.t3_bs = per; A.acc_bs = in_bs; A.out_bs = out_bs; A.e_bs = 0;
+    A.scal = P->pqinv[nd - 1] + (size_t)level * P->n_main * 2; A.sstride = 2;
+    A.nt = nt; A.nacc = ext; A.ne = 0;
+    A.nbatch = batch;
+    A.bpc = 1;
+    dim3 grid(nt * groups, 1, batch);
+    { lf_smem_optin(k_moddown_out<L1, L2, EPI_KS>, smR); LF_LAUNCH_CHECK(lf_launch(k_moddown_out<L1, L2, EPI_KS>, dim3(grid), dim3(S::TRR), smR, s, 1, A, dv)); }
+    LF_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
 extern "C" {
 
 int lf_set_bconv_engine(int engine) {
@@ -2165,6 +2224,20 @@ size_t lf_moddown_workspace_bytes(const lf_ctx* ctx, int level, int batch) {
   if (ks_check(ctx, level)) return 0;
   return (2 * (size_t)ctx->ks->n_special + 2 * (size_t)(level + 1)) * ctx->N * 4 *
          (size_t)(batch < 1 ? 1 : batch);
+}
+
+int lf_moddown_ext_rescale(const lf_ctx* ctx, int level, int ndrop, const uint32_t* in_ext, size_t in_bstride,
+                           uint32_t* out, size_t out_bstride, int batch, void* workspace, void* stream) {
+  if (int e = ks_check(ctx, level)) return e;
+  if (!in_ext || !out || !workspace || batch < 1) { lf_set_error("lf_moddown_ext_rescale: bad argument"); return 1; }
+  if (ndrop < 1 || ndrop > 2 || level < ndrop) {
+    lf_set_error("lf_moddown_ext_rescale: cannot drop %d primes at level %d", ndrop, level);
+    return 2;
+  }
+#define LF_MDR(A, B) { if (int e = moddown_rescale_pipeline<A, B>(ctx, level, ndrop, in_ext, in_bstride, out, out_bstride, batch, workspace, (cudaStream_t)stream)) return e; }
+  LF_DISPATCH_LOGN(ctx->logN, LF_MDR)
+#undef LF_MDR
+  return 0;
 }
 
 int lf_moddown_ext(const lf_ctx* ctx, int level, const uint32_t* in_ext, size_t in_bstride,
