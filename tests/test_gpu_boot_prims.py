@@ -208,3 +208,32 @@ def test_mul_rescale_list_equals_pairs(env):
     g1 = be.mul_rescale2_many([single])[0]
     w1 = be.mul_rescale2(*single)
     assert np.array_equal(g1.b.numpy(), w1.b.numpy()) and np.array_equal(g1.a.numpy(), w1.a.numpy())
+
+
+def test_moddown_ext_rescale_equals_moddown_then_rescales(env):
+    """lf_moddown_ext_rescale (ModDown and nd rescales as one division) equals lf_moddown_ext
+    followed by nd rescales, residue for residue, on hoisted extended-basis rotations."""
+    import torch
+    B, O, p, P, sk, rlk, ko, rk, rko, steps, ct, cto = env
+    from paper_2512_11269_b200 import _native
+    from paper_2512_11269_b200 import bootstrap as BT
+    from paper_2512_11269_b200.context import dptr, get_context, stream_handle
+    be = BT.GpuBackend(p, rlk, None, rk)
+    ext = be.rotate_hoisted_ext(ct, steps)                        # ExtCt, data (2, ext, N)
+    inner = torch.stack([e.data for e in ext])
+    G, level, N = inner.shape[0], ext[0].level, p.N
+    ctx = get_context(p)
+    lib = _native.lib()
+    ws = torch.empty(lib.lf_moddown_workspace_bytes(ctx.handle, level, G) // 4, dtype=torch.int32, device="cuda")
+    plain = torch.empty((G, 2, level + 1, N), dtype=torch.int32, device="cuda")
+    _native.check(lib.lf_moddown_ext(ctx.handle, level, dptr(inner), inner[0].numel(), dptr(plain),
+                                     plain[0].numel(), G, dptr(ws), stream_handle()), "lf_moddown_ext")
+    for nd in (1, 2):
+        fused = torch.empty((G, 2, level + 1 - nd, N), dtype=torch.int32, device="cuda")
+        _native.check(lib.lf_moddown_ext_rescale(ctx.handle, level, nd, dptr(inner), inner[0].numel(), dptr(fused),
+                                                 fused[0].numel(), G, dptr(ws), stream_handle()),
+                      "lf_moddown_ext_rescale")
+        want = BT.CtBatch(plain, 1, level)
+        want = be.rescale2(want) if nd == 2 else BT.CtBatch(torch.stack(
+            [torch.stack([c.b.limbs, c.a.limbs]) for c in (be.rescale(x) for x in be.unstack(want))]), 1, level - 1)
+        assert torch.equal(fused, want.data)
