@@ -2447,18 +2447,32 @@ extern "C" {
 struct lf_shard {
   const LfCtx* ctx;
   LfShardPlan* plan;
+  cudaStream_t comm_stream;     // the all-gathers of an overlapped (two half-batch) keyswitch
+  cudaEvent_t ev[8];
 };
 
 int lf_shard_create(const lf_ctx* ctx, int k, int rank, lf_shard** out) {
   if (!ctx || !out) { lf_set_error("lf_shard_create: null argument"); return 1; }
   LfShardPlan* P = nullptr;
   if (int e = lf_build_shard_plan(ctx, k, rank, &P)) return e;
-  *out = new lf_shard{ctx, P};
+  lf_shard* sh = new lf_shard{ctx, P, nullptr, {}};
+  if (cudaStreamCreateWithFlags(&sh->comm_stream, cudaStreamNonBlocking) != cudaSuccess) sh->comm_stream = nullptr;
+  for (int i = 0; i < 8 && sh->comm_stream; ++i)
+    if (cudaEventCreateWithFlags(&sh->ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaEventDestroy(sh->ev[j]);
+      cudaStreamDestroy(sh->comm_stream);
+      sh->comm_stream = nullptr;
+    }
+  *out = sh;
   return 0;
 }
 
 int lf_shard_destroy(lf_shard* sh) {
   if (!sh) return 0;
+  if (sh->comm_stream) {
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(sh->ev[i]);
+    cudaStreamDestroy(sh->comm_stream);
+  }
   lf_free_shard_plan(sh->plan);
   delete sh;
   return 0;
@@ -2476,7 +2490,13 @@ int lf_shard_info(const lf_shard* sh, int level, int* n_main, int* n_ext, int* n
 
 size_t lf_shard_ws_bytes(const lf_shard* sh, int level, int batch) {
   if (!sh || level < 0 || level > sh->plan->L || batch < 1) return 0;
-  return shard_ws_words(sh->ctx, sh->plan, level, batch) * 4;
+  size_t w = shard_ws_words(sh->ctx, sh->plan, level, batch);
+  if (batch >= 2) {            // two half-batch workspaces of the overlapped schedule
+    const int h0 = (batch + 1) / 2;
+    const size_t w2 = shard_ws_words(sh->ctx, sh->plan, level, h0) + shard_ws_words(sh->ctx, sh->plan, level, batch - h0);
+    w = w2 > w ? w2 : w;
+  }
+  return w * 4;
 }
 
 int lf_shard_gather_layout(const lf_shard* sh, int level, int batch, size_t* out6) {
@@ -2548,28 +2568,84 @@ int lf_shard_attach_comm(lf_shard* sh, lf_comm* comm) {
   return 0;
 }
 
+static int shard_gather(const lf_shard* sh, const ShardWs& w, bool modup, cudaStream_t s) {
+  lf_comm* cm = (lf_comm*)sh->plan->comm;
+  const size_t rb = (size_t)sh->ctx->N * 4;
+  const void* src = modup ? w.T0s : w.T2s;
+  void* dst = modup ? w.T0g : w.T2g;
+  const size_t bytes = (modup ? w.t0_rows : w.t2_rows) * rb;
+  if (cm) {
+    ncclResult_t r = nccl().all_gather(src, dst, bytes, ncclUint8, cm->comm, s);
+    if (r != ncclSuccess) { lf_set_error("ncclAllGather (%s): %s", modup ? "ModUp" : "ModDown", nccl().err(r)); return 3; }
+  } else if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    lf_set_error("sharded keyswitch: copy failed"); return 3;
+  }
+  return 0;
+}
+
+// One limb-sharded keyswitch / hom_mul / rotation batch.  Batches of two or more run as two
+// half-batches whose all-gathers go on the shard's comm stream, so each half's exchange overlaps
+// the other half's kernels (phase 0 h0 | gather h0 + phase 0 h1 | phase 1 h0 + gather h1 | ...);
+// the NCCL calls are issued in the same order on every rank.
 int lf_shard_keyswitch(const lf_shard* sh, const lf_shard_call* call, void* ws, void* stream) {
   if (int e = shard_check(sh, call, ws)) return e;
   lf_comm* cm = (lf_comm*)sh->plan->comm;
   if (!cm && sh->plan->k > 1) { lf_set_error("lf_shard_keyswitch: no communicator attached (lf_shard_attach_comm)"); return 2; }
   cudaStream_t s = (cudaStream_t)stream;
-  const ShardWs w = shard_carve(sh->ctx, sh->plan, call->level, call->batch, ws);
-  const size_t rb = (size_t)sh->ctx->N * 4;
-  if (int e = run_shard_phase(sh->ctx, sh->plan, 0, call, ws, s)) return e;
-  if (cm) {
-    ncclResult_t r = nccl().all_gather(w.T0s, w.T0g, w.t0_rows * rb, ncclUint8, cm->comm, s);
-    if (r != ncclSuccess) { lf_set_error("ncclAllGather (ModUp): %s", nccl().err(r)); return 3; }
-  } else if (cudaMemcpyAsync(w.T0g, w.T0s, w.t0_rows * rb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
-    lf_set_error("sharded keyswitch: copy failed"); return 3;
+  if (call->batch < 2 || !sh->comm_stream) {
+    const ShardWs w = shard_carve(sh->ctx, sh->plan, call->level, call->batch, ws);
+    if (int e = run_shard_phase(sh->ctx, sh->plan, 0, call, ws, s)) return e;
+    if (int e = shard_gather(sh, w, true, s)) return e;
+    if (int e = run_shard_phase(sh->ctx, sh->plan, 1, call, ws, s)) return e;
+    if (int e = shard_gather(sh, w, false, s)) return e;
+    return run_shard_phase(sh->ctx, sh->plan, 2, call, ws, s);
   }
-  if (int e = run_shard_phase(sh->ctx, sh->plan, 1, call, ws, s)) return e;
-  if (cm) {
-    ncclResult_t r = nccl().all_gather(w.T2s, w.T2g, w.t2_rows * rb, ncclUint8, cm->comm, s);
-    if (r != ncclSuccess) { lf_set_error("ncclAllGather (ModDown): %s", nccl().err(r)); return 3; }
-  } else if (cudaMemcpyAsync(w.T2g, w.T2s, w.t2_rows * rb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
-    lf_set_error("sharded keyswitch: copy failed"); return 3;
-  }
-  return run_shard_phase(sh->ctx, sh->plan, 2, call, ws, s);
+  const int h0 = (call->batch + 1) / 2;
+  lf_shard_call c[2] = {*call, *call};
+  c[0].batch = h0;
+  c[1].batch = call->batch - h0;
+  if (call->x) c[1].x = call->x + (size_t)h0 * call->x_bstride;
+  if (call->x2) c[1].x2 = call->x2 + (size_t)h0 * call->x_bstride;
+  if (call->out) c[1].out = call->out + (size_t)h0 * call->out_bstride;
+  if (call->e0) c[1].e0 = call->e0 + (size_t)h0 * call->e_bstride;
+  if (call->e1) c[1].e1 = call->e1 + (size_t)h0 * call->e_bstride;
+  c[1].keys = call->keys + h0;
+  if (call->galois) c[1].galois = call->galois + h0;
+  void* wsp[2] = {ws, (u32*)ws + shard_ws_words(sh->ctx, sh->plan, call->level, h0)};
+  ShardWs w[2];
+  for (int h = 0; h < 2; ++h) w[h] = shard_carve(sh->ctx, sh->plan, call->level, c[h].batch, wsp[h]);
+  cudaStream_t cs = sh->comm_stream;
+  cudaEvent_t* ev = const_cast<cudaEvent_t*>(sh->ev);
+#define LF_SH(x) do { if (int e__ = (x)) return e__; } while (0)
+#define LF_CU(x) do { if ((x) != cudaSuccess) { lf_set_error("sharded keyswitch: stream sync failed"); return 3; } } while (0)
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 0, &c[0], wsp[0], s));
+  LF_CU(cudaEventRecord(ev[0], s)); LF_CU(cudaStreamWaitEvent(cs, ev[0], 0));
+  LF_SH(shard_gather(sh, w[0], true, cs));                                   // gather 1 of h0
+  LF_CU(cudaEventRecord(ev[1], cs));
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 0, &c[1], wsp[1], s));
+  LF_CU(cudaEventRecord(ev[2], s));
+  LF_CU(cudaStreamWaitEvent(s, ev[1], 0));
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 1, &c[0], wsp[0], s));
+  LF_CU(cudaEventRecord(ev[3], s));
+  LF_CU(cudaStreamWaitEvent(cs, ev[2], 0));
+  LF_SH(shard_gather(sh, w[1], true, cs));                                   // gather 1 of h1
+  LF_CU(cudaEventRecord(ev[4], cs));
+  LF_CU(cudaStreamWaitEvent(cs, ev[3], 0));
+  LF_SH(shard_gather(sh, w[0], false, cs));                                  // gather 2 of h0
+  LF_CU(cudaEventRecord(ev[5], cs));
+  LF_CU(cudaStreamWaitEvent(s, ev[4], 0));
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 1, &c[1], wsp[1], s));
+  LF_CU(cudaEventRecord(ev[6], s));
+  LF_CU(cudaStreamWaitEvent(s, ev[5], 0));
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 2, &c[0], wsp[0], s));
+  LF_CU(cudaStreamWaitEvent(cs, ev[6], 0));
+  LF_SH(shard_gather(sh, w[1], false, cs));                                  // gather 2 of h1
+  LF_CU(cudaEventRecord(ev[7], cs));
+  LF_CU(cudaStreamWaitEvent(s, ev[7], 0));
+  LF_SH(run_shard_phase(sh->ctx, sh->plan, 2, &c[1], wsp[1], s));
+#undef LF_SH
+#undef LF_CU
+  return 0;
 }
 
 }  // extern "C"

@@ -155,3 +155,50 @@ def test_library_nccl_communicator_single_rank(env):
     finally:
         if started:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 5])
+def test_overlapped_half_batches(env, batch):
+    """lf_shard_keyswitch splits batches of two or more into two halves whose all-gathers run on
+    the shard's comm stream under the other half's kernels (k = 1: the gathers are copies).  Odd
+    batches (uneven halves), hom_mul and rotation, eager and replayed from a CUDA graph, all equal
+    the single-device pipeline."""
+    import torch
+    from paper_2512_11269_b200 import fused
+    from paper_2512_11269_b200.ntt_host import galois_element
+    from paper_2512_11269_b200.shard import ShardEngine
+    name, B, p, rlk, rk = env
+    level = p.max_level - 1
+    e = ShardEngine(p, 1, 0)
+    xs = _rand(p, level, (batch,), 20 + batch)
+    want = fused.keyswitch_batch(p, level, xs, rlk)
+    assert torch.equal(e.keyswitch(level, xs, e.shard_key(rlk)), want)
+    c1, c2 = _rand(p, level, (batch, 2), 30), _rand(p, level, (batch, 2), 31)
+    E = B.Domain.EVAL
+    ids = tuple(range(level + 1))
+    mk = lambda t: B.Ciphertext(B.RnsPolynomial(t[0], E, ids), B.RnsPolynomial(t[1], E, ids), p.scale, level)
+    steps = [(1, 5)[i % 2] for i in range(batch)]
+    gs = [galois_element(p.N, s) for s in steps]
+    kl = {s: e.shard_key(rk[s]) for s in (1, 5)}
+    got_mul = e.hom_mul(level, c1, c2, e.shard_key(rlk))
+    got_rot = e.rotate(level, c1, gs, [kl[s] for s in steps])
+    for i in range(batch):
+        wm = B.hom_mul(mk(c1[i]), mk(c2[i]), rlk, p)
+        wr = B.hom_rotate(mk(c1[i]), steps[i], rk[steps[i]], p)
+        assert torch.equal(got_mul[i, 0], wm.b.limbs) and torch.equal(got_mul[i, 1], wm.a.limbs)
+        assert torch.equal(got_rot[i, 0], wr.b.limbs) and torch.equal(got_rot[i, 1], wr.a.limbs)
+    # the fork/join through the comm stream is capturable
+    call, out = e.hom_mul_call(level, c1, c2, e.shard_key(rlk))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        e.run(call, level, batch)                     # allocate the stream's workspace outside capture
+        out.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            e.run(call, level, batch)
+    torch.cuda.current_stream().wait_stream(s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, got_mul)
