@@ -675,6 +675,12 @@ struct KsInnerArgs {
 #ifndef LF_KSI_MINB
 #define LF_KSI_MINB 2
 #endif
+#ifndef LF_KSI_PF
+// L1 prefetch one digit ahead: 1 the piece line, 2 the key lines.  Keys are read by every
+// instance of the batch (L2-resident); prefetching them into L1 as well evicts the pieces:
+// 30.9 us (1) against 31.7 (3), 32.1 (0), 32.4 (2) per C2 keyswitch at batch 32.
+#define LF_KSI_PF 1
+#endif
 // GMODE 0: no automorphism; 1: sigma_g applied to every digit's piece line before the MAC;
 // 2: permuted keys (keys stored as K o sigma_g^-1, lf_permute_rotation_key): the MAC runs in
 //    the source frame on unpermuted lines, and only the two accumulators are permuted at the end.
@@ -726,10 +732,12 @@ k_ks_inner(KsInnerArgs A, LfDev dv) {
   auto prefetch_digit = [&](int j) {
     if (j >= A.beta) return;
     const size_t lo = ((size_t)hk << L2) + (size_t)tl * C::E;
-    if (j != own_j || A.pre)
+    if ((LF_KSI_PF & 1) && (j != own_j || A.pre))
       prefetch_l1(A.T1 + b * A.t1_bs + ((size_t)(j * ext + r) << logN) + ((size_t)hs << L2) + (size_t)tl * C::E);
-    prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + kr) << logN) + lo);
-    prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + kr) << logN) + lo);
+    if (LF_KSI_PF & 2) {
+      prefetch_l1(keyb + (((size_t)(j * 2 + 0) * A.R + kr) << logN) + lo);
+      prefetch_l1(keyb + (((size_t)(j * 2 + 1) * A.R + kr) << logN) + lo);
+    }
   };
   __shared__ unsigned long long twbar;
   lf_pdl_trigger();
